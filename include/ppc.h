@@ -1,0 +1,198 @@
+/* ppc.h — pipeline-parallel stage-boundary transfer for B200 (sm_100a).  C ABI.
+ *
+ * The path (§2.2): per micro-batch, stage s sends its activation to
+ * stage s+1 (FWD) and stage s+1 later sends the activation-gradient back (BWD), under a
+ * non-interleaved 1F1B schedule (BASELINE.json north_star).  The paper's
+ * Device-Direct idea — "the host manages control operations ... the data path remains
+ * entirely on-device" — is rebuilt as sm_100a kernels that write the user buffer
+ * straight into the receiver's ring slot over NVLink 5 (one pass; the paper's
+ * user->chunk D2D, GDR, RDMA and chunk->user copies collapse into one peer write plus a
+ * chunk-pipelined receiver copy-out).  Events (flags, credits) are handled on device;
+ * the host thread only enqueues.
+ *
+ * Conventions
+ *  - Every call runs on the calling host thread and never blocks on the GPU (stream
+ *    ordered, like NCCL) unless stated.  Every call returns ppc_status_t; no exception
+ *    crosses the ABI.  A ppc_comm_t is not thread-safe.
+ *  - Pointers: "device" = CUDA device pointer on the comm's device; "host" = ordinary or
+ *    pinned host memory.  Buffers stay owned by the caller and must stay valid until the
+ *    stream reaches the operation (NCCL semantics).  libppc owns its rings, flags,
+ *    credits, NCCL communicators and IPC mappings (allocated with cudaMalloc, outside any
+ *    caching allocator, so CUDA IPC handles name whole allocations).
+ *  - Errors: argument/state errors return synchronously and enqueue nothing.
+ *    Device-detected errors (SIZE_MISMATCH, ORDER, TIMEOUT) latch a sticky error word
+ *    in mapped host memory; ppc_poll returns it and every later call fails with
+ *    PPC_ERR_STATE.  Recovery = ppc_disconnect on every rank, a caller barrier,
+ *    ppc_destroy, then a fresh ppc_create.
+ *  - Every device wait is bounded by cfg.timeout_ns (%globaltimer); no unbounded spin
+ *    (§4.3: "training frequently encountered hang issues").
+ */
+#ifndef PPC_H_
+#define PPC_H_
+
+#include <stddef.h>
+#include <cuda_runtime_api.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PPC_OK = 0,
+  PPC_ERR_INVALID_ARG = 1,       /* null pointer, bad dir, mb < 0, misconfigured cfg           */
+  PPC_ERR_GRID_MISMATCH = 2,     /* tp*pp*dp != world      */
+  PPC_ERR_RANK_OUT_OF_RANGE = 3, /* rank not in [0, world)       */
+  PPC_ERR_SELF_SEND = 4,         /* a PP neighbour's blob names the caller's own rank */
+  PPC_ERR_NO_NEIGHBOR = 5,       /* FWD send on the last stage / BWD send on stage 0           */
+  PPC_ERR_TOO_LARGE = 6,         /* bytes > cfg.max_msg_bytes                                   */
+  PPC_ERR_SIZE_MISMATCH = 7,     /* async: header bytes != recv bytes      */
+  PPC_ERR_ORDER = 8,             /* async: header seq/mb != expected (exactly once, in order)  */
+  PPC_ERR_TIMEOUT = 9,           /* async: a bounded device wait expired      */
+  PPC_ERR_BACKEND = 10,          /* DCBS rule: custom path requested for TP/DP      */
+  PPC_ERR_CUDA = 11,
+  PPC_ERR_NCCL = 12,
+  PPC_ERR_STATE = 13,            /* not connected, destroyed, or poisoned by an async error    */
+  PPC_ERR_WOULD_BLOCK = 14       /* virtual-stage (same-process) mode only: the matching send /
+                                    the slot's previous recv is not enqueued yet; nothing was
+                                    enqueued, retry after enqueueing the peer's op            */
+} ppc_status_t;
+
+typedef enum { PPC_FWD = 0, PPC_BWD = 1 } ppc_dir_t;     /* FWD: s -> s+1 ; BWD: s+1 -> s */
+typedef enum { PPC_ENGINE_SM = 0, PPC_ENGINE_CE = 1 } ppc_engine_t;
+typedef enum { PPC_GROUP_TP = 0, PPC_GROUP_DP = 1, PPC_GROUP_PP = 2 } ppc_group_t;
+typedef enum { PPC_BACKEND_NCCL = 0, PPC_BACKEND_PEER = 1, PPC_BACKEND_NONE = 2 } ppc_backend_t;
+
+typedef struct {
+  int tp, pp, dp;               /* grid; rank = pp_i*(tp*dp) + dp_i*tp + tp_i */
+  size_t max_msg_bytes;         /* ring slot payload capacity                                  */
+  int ring_slots;               /* K; 0 => 2 (double buffering)                        */
+  int channels;                 /* MPDT analogue: SM engine = CTA groups, CE engine =
+                                   copy streams; 1..8; 0 => 1                                  */
+  size_t chunk_bytes;           /* flag granularity, multiple of 4096; 0 => 1 MiB              */
+  ppc_engine_t engine;          /* data mover for sends                                        */
+  int cta_per_channel;          /* SM engine CTAs per channel; 0 => auto                       */
+  unsigned long long timeout_ns;/* bound of every device wait; 0 => 10 s                       */
+  int trace;                    /* bit 0: %globaltimer records per transfer (ppc_trace);
+                                   bit 1: CUDA-event pair around every send / recv launch on
+                                   its stream (ppc_kernel_times)                               */
+} ppc_config_t;
+
+typedef struct ppc_comm ppc_comm_t;
+
+typedef struct { int kind; /* 0 = F, 1 = B */ int mb; } ppc_op_t;
+
+typedef struct {
+  long long t_start_ns, t_end_ns;   /* %globaltimer of the first CTA start / last CTA end     */
+  int src, dst, dir, kind;          /* kind: 0 = send, 1 = recv                                */
+  long long seq, mb, bytes;
+} ppc_record_t;
+
+/* Stage compute callback of the 1F1B driver.  Enqueue work on `s` that reads `in`
+ * (in_bytes) and writes `out` (out_bytes); return 0 on success.  in == NULL on stage 0's F
+ * when no stage input is given; out may alias nothing else. */
+typedef int (*ppc_stage_fn)(void* user, int mb, const void* in, void* out,
+                            size_t in_bytes, size_t out_bytes, cudaStream_t s);
+
+/* One 1F1B step (ppc_step_1f1b).  fwd/bwd NULL => identity stage (out = in).  x/g/y/dx
+ * entries may be host or device pointers (host => copied inside the call, on stream). */
+typedef struct {
+  int M;                         /* micro-batches                                            */
+  size_t fwd_bytes, bwd_bytes;   /* boundary activation / gradient bytes per micro-batch      */
+  ppc_stage_fn fwd, bwd;
+  void* fwd_user;                /* passed to fwd                                            */
+  void* bwd_user;                /* passed to bwd                                            */
+  const void* const* x;          /* [M] stage-0 F inputs (used when s == 0), may be NULL      */
+  const void* const* g;          /* [M] last-stage B inputs (used when s == S-1), may be NULL */
+  void* const* y;                /* [M] last-stage F outputs (s == S-1), may be NULL          */
+  void* const* dx;               /* [M] stage-0 B outputs (s == 0), may be NULL               */
+} ppc_step_t;
+
+/* ---- lifecycle (§2.2 Initialization Phase) ---------------------------- */
+
+/* Resource Discovery: validate the grid (PPC_ERR_GRID_MISMATCH), allocate this rank's
+ * incoming rings (K slots x (64 B header + max_msg_bytes)), flags, credits and the mapped
+ * error word on `cuda_device`.  cuda_device = -1 creates a host-only comm (no device
+ * memory; group logic and blob exchange only — used by CPU tests). */
+ppc_status_t ppc_create(const ppc_config_t* cfg, int world, int rank, int cuda_device,
+                        ppc_comm_t** out);
+
+/* Topology Awareness blob of this rank (rank, device, PCI bus id, pid, IPC handle of the
+ * ring arena, geometry).  blob may be NULL to query *blob_bytes (fixed PPC_BLOB_BYTES). */
+#define PPC_BLOB_BYTES 512
+ppc_status_t ppc_export(ppc_comm_t* c, void* blob, size_t* blob_bytes);
+
+/* Open the PP neighbours' rings from the all-gathered blobs (world x blob_bytes, rank
+ * order) and, for TP/DP groups of size > 1, init NCCL communicators (DCBS)
+ * from nccl_ids = [tp_id, dp_id] (each 128 B, made by the group's lowest rank with
+ * ppc_nccl_unique_id).  Blobs of the same process (virtual stages on one GPU) are mapped
+ * by raw pointer instead of IPC.  n_ids = 0 skips NCCL. */
+ppc_status_t ppc_connect(ppc_comm_t* c, const void* all_blobs, size_t blob_bytes,
+                         const void* nccl_ids, int n_ids);
+
+ppc_status_t ppc_nccl_unique_id(void* out128);
+
+/* Members (rank order) and backend of this rank's group g: TP/DP -> NCCL, PP -> PEER. */
+ppc_status_t ppc_group(const ppc_comm_t* c, ppc_group_t g, int* members, int* n,
+                       ppc_backend_t* backend);
+
+/* ---- data path (§2.2 Communication Phase, Heterogeneous P2P) ----------- */
+
+/* Send `bytes` of device buffer `buf` to the PP neighbour in direction d as micro-batch
+ * `mb`.  Enqueued on `s`: waits (on device) for the slot's credit, writes the 64-B header
+ * and the payload into the neighbour's ring slot seq % K, releases per-chunk flags.
+ * Errors: PPC_ERR_NO_NEIGHBOR, PPC_ERR_TOO_LARGE, PPC_ERR_INVALID_ARG. */
+ppc_status_t ppc_pp_send(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_t bytes,
+                         long long mb, cudaStream_t s);
+
+/* Receive the next message of direction d into device buffer `buf`.  Enqueued on `s`:
+ * per chunk waits for the flag, checks the header (bytes -> SIZE_MISMATCH, seq/mb ->
+ * ORDER), copies slot -> buf, and after the last chunk returns the credit to the sender. */
+ppc_status_t ppc_pp_recv(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t bytes,
+                         long long mb, cudaStream_t s);
+
+/* Pure: the 1F1B op list of stage s (of S) over M micro-batches; ops has room for 2M.
+ * w = min(S-s-1, M) forwards, then M-w (F, B) pairs, then w backwards. */
+ppc_status_t ppc_schedule_1f1b(int S, int s, int M, ppc_op_t* ops, int* n_ops);
+
+/* One 1F1B step of this rank's stage: per op recv -> stage fn -> send, with sends on
+ * internal streams; returns after enqueueing everything on `s` (host never blocks). */
+ppc_status_t ppc_step_1f1b(ppc_comm_t* c, const ppc_step_t* st, cudaStream_t s);
+
+/* The same for S virtual stages created in this process (one GPU; ranks 0..S-1 of a
+ * pp = S grid): interleaves the stages' ops in a dependency-respecting enqueue order.
+ * comms[i], steps[i] and streams[i] belong to stage i. */
+ppc_status_t ppc_step_1f1b_local(ppc_comm_t* const* comms, int S, const ppc_step_t* steps,
+                                 const cudaStream_t* streams);
+
+/* DCBS TP/DP traffic on NCCL: in-place sum allreduce over group g.
+ * PPC_ERR_BACKEND for g == PPC_GROUP_PP. nccl_dtype is an ncclDataType_t value. */
+ppc_status_t ppc_allreduce(ppc_comm_t* c, ppc_group_t g, void* buf, size_t count,
+                           int nccl_dtype, cudaStream_t s);
+
+/* ---- diagnostics and teardown ---------------------------------------------------------- */
+ppc_status_t ppc_poll(ppc_comm_t* c);              /* non-blocking read of the error word  */
+ppc_status_t ppc_trace(ppc_comm_t* c, ppc_record_t* out, int* n);  /* synchronizes the device;
+                                                      *n in: capacity, out: records written */
+/* Device durations (ms) of the send (kind 0) or recv (kind 1) launches enqueued since the
+ * last call, from the CUDA-event pairs of cfg.trace bit 1, in launch order; synchronizes
+ * the device.  *n in: capacity, out: entries written.  Resets the list. */
+ppc_status_t ppc_kernel_times(ppc_comm_t* c, int kind, float* ms, int* n);
+ppc_status_t ppc_disconnect(ppc_comm_t* c);        /* phase 1: close peer handles, NCCL    */
+ppc_status_t ppc_destroy(ppc_comm_t* c);           /* phase 2 (after a caller barrier)     */
+const char* ppc_status_str(ppc_status_t st);
+
+/* ---- test/bench kernels (K14); not part of the transfer path --------------------------- */
+/* Fill `bytes` of device buffer with the synth/payload.py SplitMix64 stream of key
+ * (seed, step, boundary, dir, mb). */
+ppc_status_t ppc_fill_payload(void* buf, size_t bytes, int seed, int step, int boundary,
+                              int dir, long long mb, cudaStream_t s);
+/* ppc_stage_fn: out = in XOR mask(stage, dir, mb) (synth/payload.proxy_mask, seed tagged
+ * with 0x8000); `user` must point to a ppc_xor_ctx_t.  in == NULL reads zeros. */
+typedef struct { int seed, step, stage, dir; } ppc_xor_ctx_t;
+int ppc_stage_xor(void* user, int mb, const void* in, void* out, size_t in_bytes,
+                  size_t out_bytes, cudaStream_t s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PPC_H_ */

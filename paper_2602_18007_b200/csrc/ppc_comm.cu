@@ -1,0 +1,548 @@
+// libppc host side: comm lifecycle (Resource Discovery / Topology Awareness, PAPER.md
+// §2.2), DCBS groups, the pp_send / pp_recv enqueue logic
+// (P:L53), the 1F1B step driver and diagnostics.  The host only enqueues: every
+// wait on a peer happens on the device (flags/credits) or, for virtual stages sharing one
+// GPU in one process, through CUDA events.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <unistd.h>
+
+#include "ppc.h"
+#include "ppc_internal.h"
+#include "ppc_comm_impl.h"
+
+using namespace ppc;
+
+namespace {
+
+// cfg.trace bit 1: record the event opening (begin) / closing (!begin) a timed launch
+ppc_status_t time_mark(ppc_comm* c, int kind, cudaStream_t s, bool begin) {
+  if (!(c->cfg.trace & 2)) return PPC_OK;
+  std::vector<cudaEvent_t>& v = c->tev[kind];
+  size_t& n = c->tev_n[kind];
+  if (begin && n + 2 > 2 * 4096) return PPC_OK;        // list full: stop timing
+  if (!begin && (n & 1) == 0) return PPC_OK;           // begin was skipped
+  if (n == v.size()) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    v.push_back(e);
+  }
+  CK(cudaEventRecord(v[n], s));
+  ++n;
+  return PPC_OK;
+}
+
+ppc_record_t* next_record(ppc_comm* c) {
+  // the kernel that stamps the times also writes the record's metadata
+  if (!c->cfg.trace || !c->trace_dev || c->trace_n >= kTraceCap) return nullptr;
+  return c->trace_dev + c->trace_n++;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ppc_status_str(ppc_status_t st) {
+  switch (st) {
+    case PPC_OK: return "PPC_OK";
+    case PPC_ERR_INVALID_ARG: return "PPC_ERR_INVALID_ARG";
+    case PPC_ERR_GRID_MISMATCH: return "PPC_ERR_GRID_MISMATCH";
+    case PPC_ERR_RANK_OUT_OF_RANGE: return "PPC_ERR_RANK_OUT_OF_RANGE";
+    case PPC_ERR_SELF_SEND: return "PPC_ERR_SELF_SEND";
+    case PPC_ERR_NO_NEIGHBOR: return "PPC_ERR_NO_NEIGHBOR";
+    case PPC_ERR_TOO_LARGE: return "PPC_ERR_TOO_LARGE";
+    case PPC_ERR_SIZE_MISMATCH: return "PPC_ERR_SIZE_MISMATCH";
+    case PPC_ERR_ORDER: return "PPC_ERR_ORDER";
+    case PPC_ERR_TIMEOUT: return "PPC_ERR_TIMEOUT";
+    case PPC_ERR_BACKEND: return "PPC_ERR_BACKEND";
+    case PPC_ERR_CUDA: return "PPC_ERR_CUDA";
+    case PPC_ERR_NCCL: return "PPC_ERR_NCCL";
+    case PPC_ERR_STATE: return "PPC_ERR_STATE";
+    case PPC_ERR_WOULD_BLOCK: return "PPC_ERR_WOULD_BLOCK";
+  }
+  return "PPC_ERR_UNKNOWN";
+}
+
+ppc_status_t ppc_schedule_1f1b(int S, int s, int M, ppc_op_t* ops, int* n_ops) {
+  if (S < 1 || s < 0 || s >= S || M < 1 || !ops || !n_ops) return PPC_ERR_INVALID_ARG;
+  const int w = std::min(S - s - 1, M);
+  int n = 0;
+  for (int m = 0; m < w; ++m) ops[n++] = {0, m};
+  for (int i = 0; i < M - w; ++i) {
+    ops[n++] = {0, w + i};
+    ops[n++] = {1, i};
+  }
+  for (int m = M - w; m < M; ++m) ops[n++] = {1, m};
+  *n_ops = n;
+  return PPC_OK;
+}
+
+ppc_status_t ppc_create(const ppc_config_t* cfg, int world, int rank, int cuda_device,
+                        ppc_comm_t** out) {
+  if (!cfg || !out) return PPC_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (world < 1) return PPC_ERR_INVALID_ARG;
+  if (cfg->tp < 1 || cfg->pp < 1 || cfg->dp < 1 || cfg->tp * cfg->pp * cfg->dp != world)
+    return PPC_ERR_GRID_MISMATCH;
+  if (rank < 0 || rank >= world) return PPC_ERR_RANK_OUT_OF_RANGE;
+  if (cfg->ring_slots < 0 || cfg->ring_slots > kMaxSlots || cfg->channels < 0 ||
+      cfg->channels > 8 || cfg->cta_per_channel < 0 || cfg->cta_per_channel > 1024 ||
+      (cfg->engine != PPC_ENGINE_SM && cfg->engine != PPC_ENGINE_CE) ||
+      (cfg->chunk_bytes % 4096) != 0 || cfg->max_msg_bytes == 0 ||
+      cfg->max_msg_bytes > (1ull << 40))
+    return PPC_ERR_INVALID_ARG;
+  ppc_comm* c = new ppc_comm();
+  c->cfg = *cfg;
+  c->world = world;
+  c->rank = rank;
+  c->device = cuda_device;
+  c->K = cfg->ring_slots ? cfg->ring_slots : 2;
+  c->chunk = cfg->chunk_bytes ? cfg->chunk_bytes : (1u << 20);
+  c->timeout_ns = cfg->timeout_ns ? cfg->timeout_ns : 10000000000ull;
+  if (c->cfg.channels == 0) c->cfg.channels = 1;
+  const int tp = cfg->tp, dp = cfg->dp;
+  c->pp_i = rank / (tp * dp);
+  c->dp_i = (rank % (tp * dp)) / tp;
+  c->tp_i = rank % tp;
+  for (int t = 0; t < tp; ++t) c->members[PPC_GROUP_TP].push_back(c->pp_i * tp * dp + c->dp_i * tp + t);
+  for (int d = 0; d < dp; ++d) c->members[PPC_GROUP_DP].push_back(c->pp_i * tp * dp + d * tp + c->tp_i);
+  for (int p = 0; p < cfg->pp; ++p) c->members[PPC_GROUP_PP].push_back(p * tp * dp + c->dp_i * tp + c->tp_i);
+  c->lay.build(c->K, cfg->max_msg_bytes, c->chunk);
+
+  Blob& b = c->blob;
+  memset(&b, 0, sizeof(b));
+  b.magic = kBlobMagic;
+  b.version = kBlobVersion;
+  b.rank = rank;
+  b.world = world;
+  b.device = cuda_device;
+  b.pid = (int32_t)getpid();
+  b.tp = cfg->tp; b.pp = cfg->pp; b.dp = cfg->dp; b.K = c->K;
+  b.max_msg = cfg->max_msg_bytes;
+  b.chunk = c->chunk;
+  b.arena_bytes = c->lay.total;
+  b.host_hash = host_hash();
+  b.comm_ptr = (uint64_t)(uintptr_t)c;
+
+  if (cuda_device >= 0) {
+    DeviceGuard g(cuda_device);
+    auto fail = [&](ppc_status_t st) { ppc_destroy(c); return st; };
+    if (cudaSetDevice(cuda_device) != cudaSuccess) return fail(PPC_ERR_CUDA);
+    if (cudaMalloc(&c->arena, c->lay.total) != cudaSuccess) return fail(PPC_ERR_CUDA);
+    if (cudaMemset(c->arena, 0, c->lay.total) != cudaSuccess) return fail(PPC_ERR_CUDA);
+    if (cudaHostAlloc(&c->err_host, sizeof(ErrWord), cudaHostAllocMapped) != cudaSuccess)
+      return fail(PPC_ERR_CUDA);
+    memset(c->err_host, 0, sizeof(ErrWord));
+    if (cudaHostGetDevicePointer((void**)&c->err_dev, c->err_host, 0) != cudaSuccess)
+      return fail(PPC_ERR_CUDA);
+    if (cudaIpcGetMemHandle(&b.ipc, c->arena) != cudaSuccess) return fail(PPC_ERR_CUDA);
+    if (cudaDeviceGetPCIBusId(b.busid, sizeof(b.busid), cuda_device) != cudaSuccess)
+      return fail(PPC_ERR_CUDA);
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    for (int d = 0; d < 2; ++d)
+      if (cudaStreamCreateWithPriority(&c->side[d], cudaStreamNonBlocking, hi) != cudaSuccess)
+        return fail(PPC_ERR_CUDA);
+    if (cfg->engine == PPC_ENGINE_CE) {
+      for (int i = 0; i < c->cfg.channels; ++i) {
+        if (cudaStreamCreateWithPriority(&c->ce[i], cudaStreamNonBlocking, hi) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ce_join[i], cudaEventDisableTiming) != cudaSuccess)
+          return fail(PPC_ERR_CUDA);
+      }
+      if (cudaEventCreateWithFlags(&c->ce_fork, cudaEventDisableTiming) != cudaSuccess)
+        return fail(PPC_ERR_CUDA);
+    }
+    if (cfg->trace && cudaMalloc(&c->trace_dev, sizeof(ppc_record_t) * kTraceCap) != cudaSuccess)
+      return fail(PPC_ERR_CUDA);
+    if (cudaDeviceSynchronize() != cudaSuccess) return fail(PPC_ERR_CUDA);
+    b.arena_ptr = (uint64_t)(uintptr_t)c->arena;
+    b.has_arena = 1;
+  }
+  *out = c;
+  return PPC_OK;
+}
+
+ppc_status_t ppc_export(ppc_comm_t* c, void* blob, size_t* blob_bytes) {
+  if (!c || !blob_bytes) return PPC_ERR_INVALID_ARG;
+  if (!blob) {
+    *blob_bytes = PPC_BLOB_BYTES;
+    return PPC_OK;
+  }
+  if (*blob_bytes < PPC_BLOB_BYTES) return PPC_ERR_INVALID_ARG;
+  memcpy(blob, &c->blob, PPC_BLOB_BYTES);
+  *blob_bytes = PPC_BLOB_BYTES;
+  return PPC_OK;
+}
+
+ppc_status_t ppc_nccl_unique_id(void* out128) {
+  if (!out128) return PPC_ERR_INVALID_ARG;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return PPC_ERR_NCCL;
+  static_assert(sizeof(id) == 128, "nccl id");
+  memcpy(out128, &id, 128);
+  return PPC_OK;
+}
+
+static ppc_status_t map_peer(ppc_comm* c, const Blob& pb, uint8_t** base) {
+  if (!pb.has_arena) return PPC_ERR_STATE;
+  if (pb.pid == c->blob.pid && pb.host_hash == c->blob.host_hash) {
+    *base = (uint8_t*)(uintptr_t)pb.arena_ptr;      // same process: raw UVA pointer
+    return PPC_OK;
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&p, pb.ipc, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) {
+    if (getenv("PPC_DEBUG")) fprintf(stderr, "ppc: IPC open rank %d: %s\n", pb.rank, cudaGetErrorString(e));
+    return PPC_ERR_CUDA;
+  }
+  c->opened.push_back(p);
+  *base = (uint8_t*)p;
+  return PPC_OK;
+}
+
+ppc_status_t ppc_connect(ppc_comm_t* c, const void* all_blobs, size_t blob_bytes,
+                         const void* nccl_ids, int n_ids) {
+  if (!c || !all_blobs || blob_bytes != PPC_BLOB_BYTES || n_ids < 0 || n_ids > 2 ||
+      (n_ids > 0 && !nccl_ids))
+    return PPC_ERR_INVALID_ARG;
+  if (c->connected) return PPC_ERR_STATE;
+  const Blob* B = static_cast<const Blob*>(all_blobs);
+  for (int r = 0; r < c->world; ++r) {
+    const Blob& b = B[r];
+    if (b.magic != kBlobMagic || b.version != kBlobVersion || b.world != c->world ||
+        b.tp != c->cfg.tp || b.pp != c->cfg.pp || b.dp != c->cfg.dp || b.K != c->K ||
+        b.max_msg != c->cfg.max_msg_bytes || b.chunk != c->chunk)
+      return PPC_ERR_INVALID_ARG;
+    if (b.rank != r) return PPC_ERR_RANK_OUT_OF_RANGE;
+  }
+  const int tpdp = c->cfg.tp * c->cfg.dp;
+  const int prev = c->pp_i > 0 ? c->rank - tpdp : -1;
+  const int next = c->pp_i < c->cfg.pp - 1 ? c->rank + tpdp : -1;
+  for (int nb : {prev, next}) {
+    if (nb < 0) continue;
+    const Blob& pb = B[nb];
+    if (pb.comm_ptr == c->blob.comm_ptr && pb.pid == c->blob.pid &&
+        pb.host_hash == c->blob.host_hash)
+      return PPC_ERR_SELF_SEND;
+  }
+  c->ch[PPC_FWD].peer_out = next;
+  c->ch[PPC_FWD].peer_in = prev;
+  c->ch[PPC_BWD].peer_out = prev;
+  c->ch[PPC_BWD].peer_in = next;
+  if (c->device >= 0) {
+    DeviceGuard g(c->device);
+    // same-process neighbours <=> virtual stages on one GPU (events order the streams)
+    int same = 0, cross = 0;
+    for (int nb : {prev, next}) {
+      if (nb < 0) continue;
+      if (B[nb].pid == c->blob.pid && B[nb].host_hash == c->blob.host_hash) ++same; else ++cross;
+    }
+    if (same && cross) return PPC_ERR_INVALID_ARG;
+    c->local_mode = same > 0;
+    uint8_t* base_prev = nullptr;
+    uint8_t* base_next = nullptr;
+    if (prev >= 0) { ppc_status_t st = map_peer(c, B[prev], &base_prev); if (st) return st; }
+    if (next >= 0) { ppc_status_t st = map_peer(c, B[next], &base_next); if (st) return st; }
+    const Layout& L = c->lay;
+    for (int d = 0; d < 2; ++d) {
+      Chan& h = c->ch[d];
+      uint8_t* ob = (h.peer_out == next) ? base_next : base_prev;
+      uint8_t* ib = (h.peer_in == next) ? base_next : base_prev;
+      h.credit = (uint64_t*)(c->arena + L.credit[d]);
+      h.push_done = (uint32_t*)(c->arena + L.push_done[d]);
+      if (h.peer_out >= 0) {
+        h.o_payload = ob + L.payload[d];
+        h.o_hdr = (SlotHeader*)(ob + L.hdr[d]);
+        h.o_hdr_flag = (uint64_t*)(ob + L.hdr_flag[d]);
+        h.o_flags = (uint64_t*)(ob + L.flags[d]);
+        if (c->local_mode) h.out_comm = (ppc_comm*)(uintptr_t)B[h.peer_out].comm_ptr;
+      }
+      if (h.peer_in >= 0) {
+        h.i_payload = c->arena + L.payload[d];
+        h.i_hdr = (SlotHeader*)(c->arena + L.hdr[d]);
+        h.i_hdr_flag = (uint64_t*)(c->arena + L.hdr_flag[d]);
+        h.i_flags = (uint64_t*)(c->arena + L.flags[d]);
+        h.i_done = (uint32_t*)(c->arena + L.done[d]);
+        h.peer_credit = (uint64_t*)(ib + L.credit[d]);
+        if (c->local_mode) h.in_comm = (ppc_comm*)(uintptr_t)B[h.peer_in].comm_ptr;
+      }
+      if (c->local_mode) {
+        h.sent_ev.assign(c->K, nullptr);
+        h.recvd_ev.assign(c->K, nullptr);
+        for (int k = 0; k < c->K; ++k) {
+          CK(cudaEventCreateWithFlags(&h.sent_ev[k], cudaEventDisableTiming));
+          CK(cudaEventCreateWithFlags(&h.recvd_ev[k], cudaEventDisableTiming));
+        }
+      }
+    }
+    // DCBS: TP and DP groups on NCCL; PP stays on the peer kernels
+    const ncclUniqueId* ids = static_cast<const ncclUniqueId*>(nccl_ids);
+    for (int gi = 0; gi < n_ids; ++gi) {
+      const std::vector<int>& mem = c->members[gi];
+      if (mem.size() < 2) continue;
+      const int r = (int)(std::find(mem.begin(), mem.end(), c->rank) - mem.begin());
+      if (ncclCommInitRank(&c->nccl[gi], (int)mem.size(), ids[gi], r) != ncclSuccess)
+        return PPC_ERR_NCCL;
+    }
+  }
+  c->connected = true;
+  return PPC_OK;
+}
+
+ppc_status_t ppc_group(const ppc_comm_t* c, ppc_group_t g, int* members, int* n,
+                       ppc_backend_t* backend) {
+  if (!c || !n || g < PPC_GROUP_TP || g > PPC_GROUP_PP) return PPC_ERR_INVALID_ARG;
+  const std::vector<int>& m = c->members[g];
+  if (members) {
+    if (*n < (int)m.size()) return PPC_ERR_INVALID_ARG;
+    std::copy(m.begin(), m.end(), members);
+  }
+  *n = (int)m.size();
+  if (backend) *backend = g == PPC_GROUP_PP ? PPC_BACKEND_PEER : PPC_BACKEND_NCCL;
+  return PPC_OK;
+}
+
+ppc_status_t ppc_pp_send(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_t bytes,
+                         long long mb, cudaStream_t s) {
+  ppc_status_t st = check_live(c);
+  if (st) return st;
+  if (d != PPC_FWD && d != PPC_BWD) return PPC_ERR_INVALID_ARG;
+  if (mb < 0 || (bytes > 0 && !buf)) return PPC_ERR_INVALID_ARG;
+  Chan& h = c->ch[d];
+  if (h.peer_out < 0) return PPC_ERR_NO_NEIGHBOR;
+  if (bytes > c->cfg.max_msg_bytes) return PPC_ERR_TOO_LARGE;
+  if (c->device < 0) return PPC_ERR_STATE;
+  DeviceGuard g(c->device);
+  const uint64_t seq = h.send_seq + 1;
+  const int slot = (int)(seq % c->K);
+  uint64_t need = seq > (uint64_t)c->K ? seq - c->K : 0;
+  if (c->local_mode) {
+    if (need) {
+      Chan& rh = h.out_comm->ch[d];
+      if (rh.recv_seq < need) return PPC_ERR_WOULD_BLOCK;
+      CK(cudaStreamWaitEvent(s, rh.recvd_ev[slot], 0));
+    }
+    need = 0;   // ordered by the event; the kernel does not spin on the same GPU
+  }
+  const uint32_t n_chunks = (uint32_t)((bytes + c->chunk - 1) / c->chunk);
+  const int boundary = d == PPC_FWD ? c->pp_i : c->pp_i - 1;
+  ppc_record_t* rec = next_record(c);
+  uint8_t* dst = h.o_payload + (size_t)slot * c->lay.stride;
+  uint64_t* flags = h.o_flags + (size_t)slot * std::max<uint32_t>(c->lay.max_chunks, 1);
+  if (ppc_status_t ts = time_mark(c, 0, s, true)) return ts;
+  if (c->cfg.engine == PPC_ENGINE_SM || bytes == 0) {
+    PushArgs a{};
+    a.src = static_cast<const uint8_t*>(buf);
+    a.dst = dst;
+    a.hdr = h.o_hdr + slot;
+    a.hdr_flag = h.o_hdr_flag + slot;
+    a.flags = flags;
+    a.credit = h.credit;
+    a.need_credit = need;
+    a.bytes = bytes;
+    a.chunk = c->chunk;
+    a.n_chunks = n_chunks;
+    a.seq = seq;
+    a.mb = mb;
+    a.step = 0;
+    a.dir = d;
+    a.boundary = (uint32_t)boundary;
+    a.err = c->err_dev;
+    a.timeout_ns = c->timeout_ns;
+    a.rec = rec;
+    a.rec_src = c->rank;
+    a.rec_dst = h.peer_out;
+    a.done = h.push_done;
+    CK(launch_push(a, push_grid(c, n_chunks), s));
+  } else {
+    CeHeadArgs a{};
+    a.hdr = h.o_hdr + slot;
+    a.hdr_flag = h.o_hdr_flag + slot;
+    a.credit = h.credit;
+    a.need_credit = need;
+    a.bytes = bytes;
+    a.seq = seq;
+    a.step = 0;
+    a.mb = mb;
+    a.dir = d;
+    a.boundary = (uint32_t)boundary;
+    a.err = c->err_dev;
+    a.timeout_ns = c->timeout_ns;
+    a.rec = rec;
+    a.rec_src = c->rank;
+    a.rec_dst = h.peer_out;
+    CK(launch_ce_head(a, s));
+    CK(cudaEventRecord(c->ce_fork, s));
+    const int C = std::min<int>(c->cfg.channels, (int)n_chunks);
+    for (int i = 0; i < C; ++i) {
+      const uint32_t c0 = (uint32_t)((uint64_t)n_chunks * i / C);
+      const uint32_t c1 = (uint32_t)((uint64_t)n_chunks * (i + 1) / C);
+      const size_t off = (size_t)c0 * c->chunk;
+      const size_t len = std::min<size_t>((size_t)c1 * c->chunk, bytes) - off;
+      CK(cudaStreamWaitEvent(c->ce[i], c->ce_fork, 0));
+      CK(cudaMemcpyAsync(dst + off, static_cast<const uint8_t*>(buf) + off, len,
+                         cudaMemcpyDeviceToDevice, c->ce[i]));
+      CK(launch_ce_flags(flags, c0, c1, seq, i == C - 1 ? rec : nullptr, c->ce[i]));
+      CK(cudaEventRecord(c->ce_join[i], c->ce[i]));
+      CK(cudaStreamWaitEvent(s, c->ce_join[i], 0));
+    }
+  }
+  if (ppc_status_t ts = time_mark(c, 0, s, false)) return ts;
+  h.send_seq = seq;
+  if (c->local_mode) CK(cudaEventRecord(h.sent_ev[slot], s));
+  return PPC_OK;
+}
+
+ppc_status_t ppc_pp_recv(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t bytes, long long mb,
+                         cudaStream_t s) {
+  ppc_status_t st = check_live(c);
+  if (st) return st;
+  if (d != PPC_FWD && d != PPC_BWD) return PPC_ERR_INVALID_ARG;
+  if (mb < 0 || (bytes > 0 && !buf)) return PPC_ERR_INVALID_ARG;
+  Chan& h = c->ch[d];
+  if (h.peer_in < 0) return PPC_ERR_NO_NEIGHBOR;
+  if (bytes > c->cfg.max_msg_bytes) return PPC_ERR_TOO_LARGE;
+  if (c->device < 0) return PPC_ERR_STATE;
+  DeviceGuard g(c->device);
+  const uint64_t seq = h.recv_seq + 1;
+  const int slot = (int)(seq % c->K);
+  if (c->local_mode) {
+    Chan& sh = h.in_comm->ch[d];
+    if (sh.send_seq < seq) return PPC_ERR_WOULD_BLOCK;
+    CK(cudaStreamWaitEvent(s, sh.sent_ev[slot], 0));
+  }
+  const uint32_t n_chunks = (uint32_t)((bytes + c->chunk - 1) / c->chunk);
+  RecvArgs a{};
+  a.dst = static_cast<uint8_t*>(buf);
+  a.src = h.i_payload + (size_t)slot * c->lay.stride;
+  a.hdr = h.i_hdr + slot;
+  a.hdr_flag = h.i_hdr_flag + slot;
+  a.flags = h.i_flags + (size_t)slot * std::max<uint32_t>(c->lay.max_chunks, 1);
+  a.peer_credit = h.peer_credit;
+  a.done = h.i_done + slot;
+  a.bytes = bytes;
+  a.chunk = c->chunk;
+  a.n_chunks = n_chunks;
+  a.seq = seq;
+  a.mb = mb;
+  a.err = c->err_dev;
+  a.timeout_ns = c->timeout_ns;
+  a.rec = next_record(c);
+  a.rec_src = h.peer_in;
+  a.rec_dst = c->rank;
+  if (ppc_status_t ts = time_mark(c, 1, s, true)) return ts;
+  CK(launch_recv(a, recv_grid(c, n_chunks), s));
+  if (ppc_status_t ts = time_mark(c, 1, s, false)) return ts;
+  h.recv_seq = seq;
+  if (c->local_mode) CK(cudaEventRecord(h.recvd_ev[slot], s));
+  return PPC_OK;
+}
+
+ppc_status_t ppc_allreduce(ppc_comm_t* c, ppc_group_t g, void* buf, size_t count,
+                           int nccl_dtype, cudaStream_t s) {
+  ppc_status_t st = check_live(c);
+  if (st) return st;
+  if (g == PPC_GROUP_PP) return PPC_ERR_BACKEND;      // DCBS: PP is not a collective group
+  if (g != PPC_GROUP_TP && g != PPC_GROUP_DP) return PPC_ERR_INVALID_ARG;
+  if (count && !buf) return PPC_ERR_INVALID_ARG;
+  if (c->members[g].size() < 2 || count == 0) return PPC_OK;    // group of one: identity
+  if (!c->nccl[g]) return PPC_ERR_STATE;
+  DeviceGuard gd(c->device);
+  if (ncclAllReduce(buf, buf, count, (ncclDataType_t)nccl_dtype, ncclSum, c->nccl[g], s) !=
+      ncclSuccess)
+    return PPC_ERR_NCCL;
+  return PPC_OK;
+}
+
+ppc_status_t ppc_poll(ppc_comm_t* c) {
+  if (!c) return PPC_ERR_INVALID_ARG;
+  if (!c->err_host) return PPC_OK;
+  const unsigned code = ((volatile ErrWord*)c->err_host)->code;
+  if (code) c->poisoned = true;
+  return (ppc_status_t)code;
+}
+
+ppc_status_t ppc_trace(ppc_comm_t* c, ppc_record_t* out, int* n) {
+  if (!c || !n || (*n > 0 && !out)) return PPC_ERR_INVALID_ARG;
+  if (!c->trace_dev) { *n = 0; return PPC_OK; }
+  DeviceGuard g(c->device);
+  CK(cudaDeviceSynchronize());
+  const int k = std::min(*n, c->trace_n);
+  if (k > 0) CK(cudaMemcpy(out, c->trace_dev, sizeof(ppc_record_t) * k, cudaMemcpyDeviceToHost));
+  *n = k;
+  return PPC_OK;
+}
+
+ppc_status_t ppc_kernel_times(ppc_comm_t* c, int kind, float* ms, int* n) {
+  if (!c || !n || (kind != 0 && kind != 1) || (*n > 0 && !ms)) return PPC_ERR_INVALID_ARG;
+  if (c->device < 0) { *n = 0; return PPC_OK; }
+  DeviceGuard g(c->device);
+  CK(cudaDeviceSynchronize());
+  const int pairs = (int)(c->tev_n[kind] / 2);
+  const int k = std::min(*n, pairs);
+  for (int i = 0; i < k; ++i)
+    CK(cudaEventElapsedTime(&ms[i], c->tev[kind][2 * i], c->tev[kind][2 * i + 1]));
+  c->tev_n[kind] = 0;
+  *n = k;
+  return PPC_OK;
+}
+
+ppc_status_t ppc_disconnect(ppc_comm_t* c) {
+  if (!c) return PPC_ERR_INVALID_ARG;
+  DeviceGuard g(c->device);
+  if (c->device >= 0) cudaDeviceSynchronize();
+  for (int i = 0; i < 2; ++i)
+    if (c->nccl[i]) { ncclCommDestroy(c->nccl[i]); c->nccl[i] = nullptr; }
+  for (void* p : c->opened) cudaIpcCloseMemHandle(p);
+  c->opened.clear();
+  for (int d = 0; d < 2; ++d) {
+    for (cudaEvent_t e : c->ch[d].sent_ev) if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->ch[d].recvd_ev) if (e) cudaEventDestroy(e);
+    c->ch[d].sent_ev.clear();
+    c->ch[d].recvd_ev.clear();
+  }
+  c->connected = false;
+  return PPC_OK;
+}
+
+ppc_status_t ppc_destroy(ppc_comm_t* c) {
+  if (!c) return PPC_ERR_INVALID_ARG;
+  if (c->connected) ppc_disconnect(c);
+  if (c->device >= 0) {
+    DeviceGuard g(c->device);
+    cudaDeviceSynchronize();
+    StepBufs& sb = c->sb;
+    for (int d = 0; d < 2; ++d)
+      for (int i = 0; i < 2; ++i) {
+        if (sb.rbuf[d][i]) cudaFree(sb.rbuf[d][i]);
+        if (sb.obuf[d][i]) cudaFree(sb.obuf[d][i]);
+        if (sb.hbuf[d][i]) cudaFree(sb.hbuf[d][i]);
+        if (sb.rfree[d][i]) cudaEventDestroy(sb.rfree[d][i]);
+        if (sb.ofree[d][i]) cudaEventDestroy(sb.ofree[d][i]);
+      }
+    if (sb.ready) cudaEventDestroy(sb.ready);
+    for (int d = 0; d < 2; ++d) if (sb.join[d]) cudaEventDestroy(sb.join[d]);
+    for (int d = 0; d < 2; ++d) if (c->side[d]) cudaStreamDestroy(c->side[d]);
+    for (int i = 0; i < 8; ++i) {
+      if (c->ce[i]) cudaStreamDestroy(c->ce[i]);
+      if (c->ce_join[i]) cudaEventDestroy(c->ce_join[i]);
+    }
+    if (c->ce_fork) cudaEventDestroy(c->ce_fork);
+    if (c->trace_dev) cudaFree(c->trace_dev);
+    for (int k = 0; k < 2; ++k)
+      for (cudaEvent_t e : c->tev[k]) cudaEventDestroy(e);
+    if (c->arena) cudaFree(c->arena);
+    if (c->err_host) cudaFreeHost(c->err_host);
+  }
+  delete c;
+  return PPC_OK;
+}
+
+}  // extern "C"

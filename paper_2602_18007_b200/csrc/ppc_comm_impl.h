@@ -1,0 +1,187 @@
+// Private definitions shared by the libppc host translation units (not part of the ABI).
+#pragma once
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <unistd.h>
+
+#include "ppc.h"
+#include "ppc_internal.h"
+
+using namespace ppc;
+
+namespace ppc_impl {
+
+constexpr uint32_t kBlobMagic = 0x50504342u;   // "BCPP"
+constexpr uint32_t kBlobVersion = 1;
+constexpr size_t kAlign = 4096;
+constexpr int kTraceCap = 8192;
+
+inline size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct Blob {
+  uint32_t magic, version;
+  int32_t rank, world, device, pid;
+  int32_t tp, pp, dp, K;
+  uint64_t max_msg, chunk, arena_bytes;
+  uint64_t host_hash;
+  uint64_t arena_ptr;    // raw pointer (same-process mapping)
+  uint64_t comm_ptr;     // ppc_comm* (same-process virtual stages)
+  char busid[32];
+  cudaIpcMemHandle_t ipc;
+  int32_t has_arena;
+  uint8_t pad[PPC_BLOB_BYTES - 4 * 2 - 4 * 8 - 8 * 6 - 32 - sizeof(cudaIpcMemHandle_t) - 4];
+};
+static_assert(sizeof(Blob) == PPC_BLOB_BYTES, "blob size");
+
+// Byte offsets of this rank's shared arena (identical geometry on every rank).
+struct Layout {
+  size_t stride = 0;             // slot payload stride
+  size_t payload[2] = {}, hdr[2] = {}, hdr_flag[2] = {}, flags[2] = {}, credit[2] = {},
+         done[2] = {}, push_done[2] = {};
+  size_t total = 0;
+  uint32_t max_chunks = 0;
+  void build(int K, size_t max_msg, size_t chunk) {
+    stride = round_up(std::max<size_t>(max_msg, 1), kAlign);
+    max_chunks = (uint32_t)((max_msg + chunk - 1) / chunk);
+    size_t off = 0;
+    for (int d = 0; d < 2; ++d) { payload[d] = off; off += (size_t)K * stride; }
+    for (int d = 0; d < 2; ++d) { hdr[d] = off; off = round_up(off + (size_t)K * 64, 256); }
+    for (int d = 0; d < 2; ++d) { hdr_flag[d] = off; off = round_up(off + (size_t)K * 8, 256); }
+    for (int d = 0; d < 2; ++d) {
+      flags[d] = off;
+      off = round_up(off + (size_t)K * std::max<uint32_t>(max_chunks, 1) * 8, 256);
+    }
+    for (int d = 0; d < 2; ++d) { credit[d] = off; off += 256; }
+    for (int d = 0; d < 2; ++d) { done[d] = off; off = round_up(off + (size_t)K * 4, 256); }
+    for (int d = 0; d < 2; ++d) { push_done[d] = off; off += 256; }
+    total = round_up(off, kAlign);
+  }
+};
+
+struct Chan {
+  // sending side of direction d (we -> peer_out)
+  int peer_out = -1;
+  uint8_t* o_payload = nullptr;
+  SlotHeader* o_hdr = nullptr;
+  uint64_t* o_hdr_flag = nullptr;
+  uint64_t* o_flags = nullptr;
+  uint64_t* credit = nullptr;        // ours; the receiver writes it
+  uint32_t* push_done = nullptr;
+  uint64_t send_seq = 0;
+  ppc_comm* out_comm = nullptr;      // same-process peer
+  // receiving side of direction d (peer_in -> we)
+  int peer_in = -1;
+  uint8_t* i_payload = nullptr;
+  SlotHeader* i_hdr = nullptr;
+  uint64_t* i_hdr_flag = nullptr;
+  uint64_t* i_flags = nullptr;
+  uint32_t* i_done = nullptr;
+  uint64_t* peer_credit = nullptr;   // in the sender's arena
+  uint64_t recv_seq = 0;
+  ppc_comm* in_comm = nullptr;
+  // virtual-stage mode: stream ordering through events
+  std::vector<cudaEvent_t> sent_ev, recvd_ev;
+};
+
+struct StepBufs {
+  size_t bytes = 0;
+  uint8_t* rbuf[2][2] = {};     // [dir][i] recv landing
+  uint8_t* obuf[2][2] = {};     // [dir][i] stage output
+  uint8_t* hbuf[2][2] = {};     // [dir][i] staging for host inputs / outputs
+  cudaEvent_t rfree[2][2] = {}, ofree[2][2] = {}, ready = nullptr, join[2] = {};
+  bool rpending[2][2] = {}, opending[2][2] = {};
+};
+
+}  // namespace ppc_impl
+
+using namespace ppc_impl;
+
+struct ppc_comm {
+  ppc_config_t cfg{};
+  int world = 0, rank = 0, device = -1;
+  int pp_i = 0, dp_i = 0, tp_i = 0;
+  int K = 2;
+  size_t chunk = 1 << 20;
+  unsigned long long timeout_ns = 10000000000ull;
+  Layout lay;
+  uint8_t* arena = nullptr;
+  ErrWord* err_host = nullptr;
+  ErrWord* err_dev = nullptr;
+  bool connected = false, poisoned = false, local_mode = false;
+  Chan ch[2];
+  std::vector<void*> opened;          // IPC-opened peer arenas
+  ncclComm_t nccl[2] = {nullptr, nullptr};
+  std::vector<int> members[3];
+  cudaStream_t side[2] = {nullptr, nullptr};   // send streams of the step driver
+  cudaStream_t ce[8] = {};                     // CE engine channel streams
+  cudaEvent_t ce_fork = nullptr, ce_join[8] = {};
+  ppc_record_t* trace_dev = nullptr;
+  int trace_n = 0;
+  // cfg.trace bit 1: event pairs around send (0) / recv (1) launches
+  std::vector<cudaEvent_t> tev[2];
+  size_t tev_n[2] = {0, 0};
+  StepBufs sb;
+  Blob blob{};
+};
+
+namespace ppc_impl {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (dev >= 0) {
+      cudaGetDevice(&prev);
+      if (prev != dev) cudaSetDevice(dev); else prev = -1;
+    }
+  }
+  ~DeviceGuard() { if (prev >= 0) cudaSetDevice(prev); }
+};
+
+#define CK(x)                                                                    \
+  do {                                                                           \
+    cudaError_t e_ = (x);                                                        \
+    if (e_ != cudaSuccess) {                                                     \
+      if (getenv("PPC_DEBUG")) fprintf(stderr, "ppc: %s -> %s (%s:%d)\n", #x,     \
+                                       cudaGetErrorString(e_), __FILE__, __LINE__); \
+      return PPC_ERR_CUDA;                                                       \
+    }                                                                            \
+  } while (0)
+
+inline uint64_t host_hash() {
+  char h[256] = {};
+  gethostname(h, sizeof(h) - 1);
+  uint64_t x = 1469598103934665603ull;
+  for (char* p = h; *p; ++p) x = (x ^ (uint8_t)*p) * 1099511628211ull;
+  return x;
+}
+
+inline ppc_status_t check_live(ppc_comm* c) {
+  if (!c || !c->connected) return PPC_ERR_STATE;
+  if (c->poisoned) return PPC_ERR_STATE;
+  if (c->err_host && ((volatile ErrWord*)c->err_host)->code != 0) {
+    c->poisoned = true;
+    return PPC_ERR_STATE;
+  }
+  return PPC_OK;
+}
+
+inline int push_grid(const ppc_comm* c, uint32_t n_chunks) {
+  if (n_chunks == 0) return 1;
+  int per = c->cfg.cta_per_channel;
+  int chans = std::max(1, c->cfg.channels);
+  int g = per > 0 ? per * chans : (c->local_mode ? 296 : 32 * chans);
+  return (int)std::max<uint32_t>(1, std::min<uint32_t>(n_chunks, (uint32_t)g));
+}
+inline int recv_grid(const ppc_comm* c, uint32_t n_chunks) {
+  if (n_chunks == 0) return 1;
+  int g = c->local_mode ? 296 : 64;
+  return (int)std::max<uint32_t>(1, std::min<uint32_t>(n_chunks, (uint32_t)g));
+}
+
+}  // namespace ppc_impl

@@ -1,0 +1,105 @@
+// Internal declarations of libppc (not part of the C ABI).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "ppc.h"
+
+namespace ppc {
+
+constexpr uint32_t kMagic = 0x48435043u;     // SPEC.md S:L403 chunk-header magic, reused
+constexpr int kThreads = 512;                // CTA size of the copy kernels
+constexpr int kMaxSlots = 64;
+
+// 64-byte slot header, little-endian.
+struct __align__(64) SlotHeader {
+  uint32_t magic;
+  uint8_t dir, boundary;
+  uint16_t zero;
+  uint64_t bytes;
+  uint64_t seq;
+  int64_t mb;
+  uint64_t step;
+  uint8_t pad[24];
+};
+static_assert(sizeof(SlotHeader) == 64, "slot header is 64 B");
+
+// Error word in mapped host memory: [0] = status code, [1] = seq, [2] = dir | kind << 8.
+struct ErrWord {
+  unsigned int code, seq, info, pad;
+};
+
+struct PushArgs {
+  const uint8_t* src;
+  uint8_t* dst;                 // peer (or local) slot payload
+  SlotHeader* hdr;              // peer slot header
+  uint64_t* hdr_flag;           // peer: = seq once the header is written
+  uint64_t* flags;              // peer: flags[c] = seq once chunk c is written
+  const uint64_t* credit;       // local: last seq the receiver consumed
+  uint64_t need_credit;         // wait until credit >= need_credit (0: no wait)
+  uint64_t bytes, chunk;
+  uint32_t n_chunks;
+  uint64_t seq;
+  int64_t mb;
+  uint64_t step;
+  uint32_t dir, boundary;
+  ErrWord* err;
+  uint64_t timeout_ns;
+  ppc_record_t* rec;            // trace record or nullptr
+  int rec_src, rec_dst;
+  uint32_t* done;               // completion counter (trace only)
+};
+
+struct RecvArgs {
+  uint8_t* dst;                 // user buffer
+  const uint8_t* src;           // local slot payload
+  const SlotHeader* hdr;
+  const uint64_t* hdr_flag;
+  const uint64_t* flags;
+  uint64_t* peer_credit;        // sender's credit word (peer memory)
+  uint32_t* done;               // local completion counter of this slot
+  uint64_t bytes, chunk;
+  uint32_t n_chunks;
+  uint64_t seq;
+  int64_t mb;
+  ErrWord* err;
+  uint64_t timeout_ns;
+  ppc_record_t* rec;
+  int rec_src, rec_dst;
+};
+
+// CE engine pieces: header/credit kernel before the copies, flag kernel after each.
+struct CeHeadArgs {
+  SlotHeader* hdr;
+  uint64_t* hdr_flag;
+  const uint64_t* credit;
+  uint64_t need_credit;
+  uint64_t bytes, seq, step;
+  int64_t mb;
+  uint32_t dir, boundary;
+  ErrWord* err;
+  uint64_t timeout_ns;
+  ppc_record_t* rec;
+  int rec_src, rec_dst;
+};
+
+__device__ __forceinline__ void fill_record(ppc_record_t* r, long long t0, int src, int dst,
+                                            int dir, int kind, uint64_t seq, int64_t mb,
+                                            uint64_t bytes) {
+  r->t_start_ns = t0;
+  r->t_end_ns = 0;
+  r->src = src;
+  r->dst = dst;
+  r->dir = dir;
+  r->kind = kind;
+  r->seq = (long long)seq;
+  r->mb = mb;
+  r->bytes = (long long)bytes;
+}
+
+cudaError_t launch_push(const PushArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_recv(const RecvArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_ce_head(const CeHeadArgs& a, cudaStream_t s);
+cudaError_t launch_ce_flags(uint64_t* flags, uint32_t c0, uint32_t c1, uint64_t seq,
+                            ppc_record_t* rec, cudaStream_t s);
+
+}  // namespace ppc

@@ -1,0 +1,328 @@
+// sm_100a kernels of the stage-boundary transfer (K9 push, K10 recv, K12 CE signalling)
+// and the test kernels (K14: SplitMix64 fill, XOR stage proxy).
+//
+// Memory-ordering protocol:
+//   sender, per chunk:   data stores -> fence.acq_rel.sys (every thread) -> bar.sync ->
+//                        st.release.sys flags[c] = seq (thread 0)
+//   receiver, per chunk: ld.acquire.sys flags[c] >= seq (thread 0) -> bar.sync ->
+//                        L1-bypassing (.cg) loads of the slot
+//   credit:              receiver's last CTA -> st.release.sys credit = seq (sender memory);
+//                        sender waits ld.acquire.sys credit >= seq - K before writing a slot.
+// Flags and credits are monotone u64 sequence numbers (never reset); every wait compares
+// wrap-safe and is bounded by %globaltimer (§4.3 P:L211 hangs).
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "ppc_internal.h"
+
+namespace ppc {
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_sys() {
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+// streaming read of data nobody writes during the kernel (user source buffer)
+__device__ __forceinline__ uint4 ld_src(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+// coherent read (L2) of ring data written by another GPU / kernel
+__device__ __forceinline__ uint4 ld_ring(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p) : "memory");
+  return r;
+}
+__device__ __forceinline__ void st_data(uint4* p, const uint4& v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w) : "memory");
+}
+
+__device__ __forceinline__ void latch(ErrWord* e, unsigned code, uint64_t seq, unsigned info) {
+  // plain system-scope stores into mapped host memory; any error poisons the comm
+  volatile ErrWord* v = e;
+  v->seq = (unsigned)seq;
+  v->info = info;
+  __threadfence_system();
+  v->code = code;
+  __threadfence_system();
+}
+
+// Wait until *p >= target (wrap-safe); false on timeout.
+__device__ __forceinline__ bool wait_geq(const uint64_t* p, uint64_t target, uint64_t deadline) {
+  uint64_t v = ld_acquire_sys(p);
+  int spins = 0;
+  while ((int64_t)(v - target) < 0) {
+    if (((++spins) & 63) == 0 && globaltimer() > deadline) return false;
+    __nanosleep(32);
+    v = ld_acquire_sys(p);
+  }
+  return true;
+}
+
+// Copy `len` bytes with the CTA's threads: 16-byte vectors, UNROLL loads in flight per
+// thread before their stores; byte loop for misaligned buffers and the ragged tail.
+template <bool kRingSrc>
+__device__ __forceinline__ void cta_copy(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src,
+                                         uint64_t len) {
+  constexpr int U = 8;
+  const uint64_t tid = threadIdx.x, nt = blockDim.x;
+  uint64_t body = 0;
+  if ((((uintptr_t)dst | (uintptr_t)src) & 15) == 0) {
+    const uint64_t n16 = len >> 4;
+    const uint4* s = reinterpret_cast<const uint4*>(src);
+    uint4* d = reinterpret_cast<uint4*>(dst);
+    const uint64_t step = nt * U;
+    uint64_t i = tid;
+    for (; i + (U - 1) * nt < n16; i += step) {
+      uint4 v[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) v[j] = kRingSrc ? ld_ring(s + i + j * nt) : ld_src(s + i + j * nt);
+#pragma unroll
+      for (int j = 0; j < U; ++j) st_data(d + i + j * nt, v[j]);
+    }
+    for (; i < n16; i += nt) st_data(d + i, kRingSrc ? ld_ring(s + i) : ld_src(s + i));
+    body = n16 << 4;
+  }
+  for (uint64_t k = body + tid; k < len; k += nt) {
+    uint8_t b;
+    if (kRingSrc) {
+      b = *reinterpret_cast<const volatile uint8_t*>(src + k);
+    } else {
+      b = src[k];
+    }
+    dst[k] = b;
+  }
+}
+
+// ---------------------------------------------------------------- K9: push (SM engine)
+__global__ void __launch_bounds__(kThreads) push_kernel(PushArgs a) {
+  uint64_t deadline = 0;
+  int fail = 0;
+  if (threadIdx.x == 0) {
+    const uint64_t t0 = globaltimer();
+    deadline = t0 + a.timeout_ns;
+    if (a.rec && blockIdx.x == 0)
+      fill_record(a.rec, (long long)t0, a.rec_src, a.rec_dst, a.dir, 0, a.seq, a.mb, a.bytes);
+    if (a.need_credit && !wait_geq(a.credit, a.need_credit, deadline)) {
+      latch(a.err, PPC_ERR_TIMEOUT, a.seq, a.dir);
+      fail = 1;
+    } else if (blockIdx.x == 0) {
+      SlotHeader h = {};
+      h.magic = kMagic;
+      h.dir = (uint8_t)a.dir;
+      h.boundary = (uint8_t)a.boundary;
+      h.bytes = a.bytes;
+      h.seq = a.seq;
+      h.mb = a.mb;
+      h.step = a.step;
+      const uint4* hs = reinterpret_cast<const uint4*>(&h);
+      uint4* hd = reinterpret_cast<uint4*>(a.hdr);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) st_data(hd + j, hs[j]);
+      st_release_sys(a.hdr_flag, a.seq);
+    }
+  }
+  if (__syncthreads_or(fail)) return;
+  for (uint32_t c = blockIdx.x; c < a.n_chunks; c += gridDim.x) {
+    const uint64_t off = (uint64_t)c * a.chunk;
+    const uint64_t len = min(a.chunk, a.bytes - off);
+    cta_copy<false>(a.dst + off, a.src + off, len);
+    fence_acq_rel_sys();            // every thread: its peer stores before the flag
+    __syncthreads();
+    if (threadIdx.x == 0) st_release_sys(a.flags + c, a.seq);
+  }
+  if (a.rec) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(a.done, 1u) == gridDim.x - 1) {
+        *a.done = 0;
+        a.rec->t_end_ns = (long long)globaltimer();
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K10: recv + copy-out
+__global__ void __launch_bounds__(kThreads) recv_kernel(RecvArgs a) {
+  uint64_t deadline = 0;
+  int fail = 0;
+  if (threadIdx.x == 0) {
+    const uint64_t t0 = globaltimer();
+    deadline = t0 + a.timeout_ns;
+    if (a.rec && blockIdx.x == 0)
+      fill_record(a.rec, (long long)t0, a.rec_src, a.rec_dst, -1, 1, a.seq, a.mb, a.bytes);
+    if (!wait_geq(a.hdr_flag, a.seq, deadline)) {
+      latch(a.err, PPC_ERR_TIMEOUT, a.seq, 0x100u);
+      fail = 1;
+    } else {
+      const volatile SlotHeader* h = a.hdr;
+      if (h->magic != kMagic || h->seq != a.seq || h->mb != a.mb) {
+        latch(a.err, PPC_ERR_ORDER, a.seq, 0x100u);
+        fail = 1;
+      } else if (h->bytes != a.bytes) {
+        latch(a.err, PPC_ERR_SIZE_MISMATCH, a.seq, 0x100u);
+        fail = 1;
+      }
+    }
+  }
+  if (__syncthreads_or(fail)) return;
+  for (uint32_t c = blockIdx.x; c < a.n_chunks; c += gridDim.x) {
+    int f = 0;
+    if (threadIdx.x == 0 && !wait_geq(a.flags + c, a.seq, deadline)) {
+      latch(a.err, PPC_ERR_TIMEOUT, a.seq, 0x100u | c << 12);
+      f = 1;
+    }
+    if (__syncthreads_or(f)) return;
+    const uint64_t off = (uint64_t)c * a.chunk;
+    const uint64_t len = min(a.chunk, a.bytes - off);
+    cta_copy<true>(a.dst + off, a.src + off, len);
+  }
+  __threadfence();                 // slot reads + user-buffer writes before the credit
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (atomicAdd(a.done, 1u) == gridDim.x - 1) {
+      *a.done = 0;                 // next use of this slot is stream-ordered after us
+      __threadfence();
+      st_release_sys(a.peer_credit, a.seq);
+      if (a.rec) a.rec->t_end_ns = (long long)globaltimer();
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K12: CE signalling
+__global__ void ce_head_kernel(CeHeadArgs a) {
+  const uint64_t t0 = globaltimer();
+  if (a.rec) fill_record(a.rec, (long long)t0, a.rec_src, a.rec_dst, a.dir, 0, a.seq, a.mb, a.bytes);
+  if (a.need_credit && !wait_geq(a.credit, a.need_credit, t0 + a.timeout_ns)) {
+    latch(a.err, PPC_ERR_TIMEOUT, a.seq, a.dir);
+    return;
+  }
+  SlotHeader h = {};
+  h.magic = kMagic;
+  h.dir = (uint8_t)a.dir;
+  h.boundary = (uint8_t)a.boundary;
+  h.bytes = a.bytes;
+  h.seq = a.seq;
+  h.mb = a.mb;
+  h.step = a.step;
+  const uint4* hs = reinterpret_cast<const uint4*>(&h);
+  uint4* hd = reinterpret_cast<uint4*>(a.hdr);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) st_data(hd + j, hs[j]);
+  st_release_sys(a.hdr_flag, a.seq);
+}
+
+// Runs after the copy engine finished this channel's bytes (stream order).
+__global__ void ce_flags_kernel(uint64_t* flags, uint32_t c0, uint32_t c1, uint64_t seq,
+                                ppc_record_t* rec) {
+  fence_acq_rel_sys();
+  for (uint32_t c = c0 + threadIdx.x; c < c1; c += blockDim.x) st_release_sys(flags + c, seq);
+  if (rec && threadIdx.x == 0) rec->t_end_ns = (long long)globaltimer();
+}
+
+cudaError_t launch_push(const PushArgs& a, int grid, cudaStream_t s) {
+  push_kernel<<<grid, kThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_recv(const RecvArgs& a, int grid, cudaStream_t s) {
+  recv_kernel<<<grid, kThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_ce_head(const CeHeadArgs& a, cudaStream_t s) {
+  ce_head_kernel<<<1, 1, 0, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_ce_flags(uint64_t* flags, uint32_t c0, uint32_t c1, uint64_t seq,
+                            ppc_record_t* rec, cudaStream_t s) {
+  ce_flags_kernel<<<1, 32, 0, s>>>(flags, c0, c1, seq, rec);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- K14: test kernels
+// SplitMix64 (synth/payload.py, implemented independently here):
+//   key = seed<<48 ^ step<<32 ^ boundary<<24 ^ dir<<23 ^ mb ; base = mix(key + G)
+//   word[w] = mix(base + (w+1)*G)
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__host__ __device__ inline uint64_t payload_key(int seed, int step, int boundary, int dir,
+                                                long long mb) {
+  return ((uint64_t)(uint32_t)seed << 48) ^ ((uint64_t)(uint32_t)step << 32) ^
+         ((uint64_t)(uint32_t)boundary << 24) ^ ((uint64_t)(uint32_t)dir << 23) ^ (uint64_t)mb;
+}
+
+// out = in XOR stream (in == nullptr: out = stream).  Whole words as u64, ragged tail bytewise.
+__global__ void splitmix_xor_kernel(uint8_t* out, const uint8_t* in, uint64_t bytes, uint64_t key) {
+  const uint64_t base = mix64(key + kGamma);
+  const uint64_t nw = bytes >> 3;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const bool aligned = ((((uintptr_t)out) | ((uintptr_t)in)) & 7) == 0;
+  for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += stride) {
+    uint64_t v = mix64(base + (w + 1) * kGamma);
+    if (aligned) {
+      if (in) v ^= reinterpret_cast<const uint64_t*>(in)[w];
+      reinterpret_cast<uint64_t*>(out)[w] = v;
+    } else {
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        uint8_t x = (uint8_t)(v >> (8 * b));
+        if (in) x ^= in[w * 8 + b];
+        out[w * 8 + b] = x;
+      }
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (bytes & 7)) {
+    const uint64_t v = mix64(base + (nw + 1) * kGamma);
+    for (uint64_t k = nw * 8; k < bytes; ++k) {
+      uint8_t x = (uint8_t)(v >> (8 * (k & 7)));
+      if (in) x ^= in[k];
+      out[k] = x;
+    }
+  }
+}
+
+}  // namespace ppc
+
+extern "C" ppc_status_t ppc_fill_payload(void* buf, size_t bytes, int seed, int step,
+                                         int boundary, int dir, long long mb, cudaStream_t s) {
+  if (bytes == 0) return PPC_OK;
+  if (!buf || seed < 0 || seed >= (1 << 16) || step < 0 || step >= (1 << 16) || boundary < 0 ||
+      boundary > 255 || (dir != 0 && dir != 1) || mb < 0 || mb >= (1ll << 23))
+    return PPC_ERR_INVALID_ARG;
+  const uint64_t nw = (bytes + 7) / 8;
+  const int grid = (int)std::min<uint64_t>((nw + 255) / 256, 148ull * 8);
+  ppc::splitmix_xor_kernel<<<grid, 256, 0, s>>>(static_cast<uint8_t*>(buf), nullptr, bytes,
+                                               ppc::payload_key(seed, step, boundary, dir, mb));
+  return cudaGetLastError() == cudaSuccess ? PPC_OK : PPC_ERR_CUDA;
+}
+
+extern "C" int ppc_stage_xor(void* user, int mb, const void* in, void* out, size_t in_bytes,
+                             size_t out_bytes, cudaStream_t s) {
+  const ppc_xor_ctx_t* c = static_cast<const ppc_xor_ctx_t*>(user);
+  if (!c || !out || (in && in_bytes != out_bytes)) return PPC_ERR_INVALID_ARG;
+  if (out_bytes == 0) return PPC_OK;
+  const uint64_t nw = (out_bytes + 7) / 8;
+  const int grid = (int)std::min<uint64_t>((nw + 255) / 256, 148ull * 8);
+  ppc::splitmix_xor_kernel<<<grid, 256, 0, s>>>(
+      static_cast<uint8_t*>(out), static_cast<const uint8_t*>(in), out_bytes,
+      ppc::payload_key(c->seed ^ 0x8000, c->step, c->stage, c->dir, mb));
+  return cudaGetLastError() == cudaSuccess ? PPC_OK : PPC_ERR_CUDA;
+}

@@ -1,0 +1,176 @@
+"""Worker for the multi-GPU parity tests (one process per GPU, launched by torchrun from
+tests/test_gpu_multi.py).  Bootstrap over gloo (the host control plane), data over the
+libppc peer kernels; each rank checks its own outputs against the oracle and exits
+non-zero on any mismatch."""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2602_18007_b200 as ppc  # noqa: E402
+from oracle.proxy import xor_closed_form  # noqa: E402
+from synth import payload as P  # noqa: E402
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy().view(np.uint8).reshape(-1)
+
+
+def buf(n):
+    return torch.empty(max(n, 1), dtype=torch.uint8, device="cuda")
+
+
+def case_sendrecv(rank, world, engine):
+    cfg = ppc.make_config(pp=world, max_msg_bytes=8 << 20, chunk_bytes=256 << 10, engine=engine,
+                          channels=4 if engine else 1)
+    comm = ppc.connect_distributed(cfg, rank, world, rank, with_nccl=False)
+    s = torch.cuda.current_stream()
+    sizes = [0, 1, 4096, 3 * (256 << 10) + 5, 8 << 20]
+    for rep in range(3):
+        for i, n in enumerate(sizes):
+            mb = rep * len(sizes) + i
+            for d in (ppc.FWD, ppc.BWD):
+                sender = rank == 0 if d == ppc.FWD else rank == 1
+                receiver = rank == 1 if d == ppc.FWD else rank == 0
+                if sender:
+                    b = buf(n)
+                    ppc.fill_payload(b, n, 42, 0, 0, d, mb)
+                    comm.send(d, b, n, mb=mb, stream=s)
+                    torch.cuda.synchronize()
+                elif receiver:
+                    b = buf(n)
+                    comm.recv(d, b, n, mb=mb, stream=s)
+                    got = host(b)[:n]
+                    want = P.payload_bytes(42, 0, 0, d, mb, n)
+                    assert np.array_equal(got, want), (rank, d, n, mb)
+    torch.cuda.synchronize()
+    assert comm.poll() == 0
+    return comm
+
+
+def case_xor(rank, world, engine, M=6):
+    S = world
+    n = 5 * (256 << 10) + 777
+    cfg = ppc.make_config(pp=S, max_msg_bytes=n, chunk_bytes=256 << 10, engine=engine,
+                          channels=2 if engine else 1, trace=1)
+    comm = ppc.connect_distributed(cfg, rank, world, rank, with_nccl=False)
+    X = [buf(n) for _ in range(M)] if rank == 0 else None
+    G = [buf(n) for _ in range(M)] if rank == S - 1 else None
+    out = [buf(n) for _ in range(M)]
+    for m in range(M):
+        if X:
+            ppc.fill_payload(X[m], n, 42, 0, P.SRC_BOUNDARY, 0, m)
+        if G:
+            ppc.fill_payload(G[m], n, 42, 0, P.SRC_BOUNDARY, 1, m)
+    fctx, bctx = ppc.XorCtx(42, 0, rank, 0), ppc.XorCtx(42, 0, rank, 1)
+    args = ppc.StepArgs(M, n, n, fwd=ppc.STAGE_XOR, bwd=ppc.STAGE_XOR, fwd_user=fctx,
+                        bwd_user=bctx, x=X, g=G, y=out if rank == S - 1 else None,
+                        dx=out if rank == 0 else None)
+    for step in range(2):                      # two steps: seq numbers continue across steps
+        ppc.step_1f1b(comm, args, torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        assert comm.poll() == 0, ppc.STATUS[comm.poll()]
+        if rank in (0, S - 1):
+            mask = lambda s, d, m: P.proxy_mask(42, 0, s, d, m, n)
+            for m in range(M):
+                y, g = xor_closed_form(S, m, P.source_activation(42, 0, m, n),
+                                       P.source_gradient(42, 0, m, n), mask)
+                want = y if rank == S - 1 else g
+                assert np.array_equal(host(out[m])[:n], want), (rank, step, m)
+    recs = [r for r in comm.trace() if r["kind"] == 1]
+    for src in (rank - 1, rank + 1):
+        rs = [r for r in recs if r["src"] == src]
+        assert [r["seq"] for r in rs] == list(range(1, len(rs) + 1))
+        assert [r["mb"] for r in rs] == list(range(M)) * (len(rs) // M)
+    return comm
+
+
+def case_timeout(rank, world):
+    cfg = ppc.make_config(pp=world, max_msg_bytes=1 << 20, timeout_ns=300_000_000)
+    comm = ppc.connect_distributed(cfg, rank, world, rank, with_nccl=False)
+    if rank == 1:
+        b = buf(4096)
+        comm.recv(ppc.FWD, b, 4096, mb=0, stream=torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        assert ppc.STATUS[comm.poll()] == "TIMEOUT", comm.poll()
+    return comm
+
+
+def case_dcbs(rank, world):
+    """PP=2 x TP=2 on 4 GPUs: TP allreduce on NCCL running beside the PP kernels."""
+    tp = 2
+    cfg = ppc.make_config(tp=tp, pp=world // tp, dp=1, max_msg_bytes=1 << 20)
+    comm = ppc.connect_distributed(cfg, rank, world, rank, with_nccl=True)
+    tp_m, be = comm.group(ppc.GROUP_TP)
+    pp_m, be2 = comm.group(ppc.GROUP_PP)
+    assert be == ppc.BACKEND_NCCL and be2 == ppc.BACKEND_PEER and len(tp_m) == tp
+    with_err = comm
+    side = torch.cuda.Stream()
+    t = torch.full((1 << 20,), float(rank + 1), device="cuda")
+    with torch.cuda.stream(side):
+        comm.allreduce(ppc.GROUP_TP, t, 7, stream=side)        # ncclFloat32 = 7
+    try:
+        comm.allreduce(ppc.GROUP_PP, t, 7)
+        raise AssertionError("PP allreduce must be refused (DCBS)")
+    except ppc.PpcError as e:
+        assert e.name == "BACKEND"
+    n = 1 << 20
+    M = 4
+    pp_rank = pp_m.index(rank)
+    X = [buf(n) for _ in range(M)] if pp_rank == 0 else None
+    G = [buf(n) for _ in range(M)] if pp_rank == len(pp_m) - 1 else None
+    for m in range(M):
+        if X:
+            ppc.fill_payload(X[m], n, 42, 0, P.SRC_BOUNDARY, 0, m)
+        if G:
+            ppc.fill_payload(G[m], n, 42, 0, P.SRC_BOUNDARY, 1, m)
+    out = [buf(n) for _ in range(M)]
+    args = ppc.StepArgs(M, n, n, x=X, g=G, y=out if G else None, dx=out if X else None)
+    ppc.step_1f1b(comm, args, torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    assert with_err.poll() == 0
+    want = sum(range(1, tp + 1)) + tp * tp_m[0]
+    assert torch.all(t == float(want)).item(), (t[0].item(), want)
+    for m in range(M):      # identity stages: stage 0 gets G_m back, last stage gets X_m
+        ref = P.source_gradient(42, 0, m, n) if X else P.source_activation(42, 0, m, n)
+        assert np.array_equal(host(out[m])[:n], ref)
+    return comm
+
+
+def main():
+    case = sys.argv[1]
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo")
+    if case == "sendrecv_sm":
+        comm = case_sendrecv(rank, world, ppc.ENGINE_SM)
+    elif case == "sendrecv_ce":
+        comm = case_sendrecv(rank, world, ppc.ENGINE_CE)
+    elif case == "xor_sm":
+        comm = case_xor(rank, world, ppc.ENGINE_SM)
+    elif case == "xor_ce":
+        comm = case_xor(rank, world, ppc.ENGINE_CE)
+    elif case == "timeout":
+        comm = case_timeout(rank, world)
+    elif case == "dcbs":
+        comm = case_dcbs(rank, world)
+    else:
+        raise SystemExit(f"unknown case {case}")
+    torch.cuda.synchronize()
+    dist.barrier()
+    comm.disconnect()
+    dist.barrier()
+    comm.destroy()
+    dist.destroy_process_group()
+    print(f"rank {rank} {case} OK", flush=True)
+
+
+if __name__ == "__main__":
+    main()

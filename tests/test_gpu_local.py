@@ -1,0 +1,167 @@
+"""GPU parity of the transfer path on one B200: virtual stages of one pipeline in one
+process (the intra-device ring, K11), through the C-ABI.  Every comparison is element by
+element against the oracle (oracle/transfer.py, oracle/proxy.py) on the same seeded
+inputs (synth/payload.py), bit-exact."""
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2602_18007_b200 as ppc
+from oracle.proxy import run_1f1b, xor_closed_form, xor_stage
+from synth import payload as P
+
+pytestmark = pytest.mark.gpu
+
+DEV = 0
+
+
+def _host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy().view(np.uint8).reshape(-1)
+
+
+def _buf(n):
+    return torch.empty(max(n, 1), dtype=torch.uint8, device=f"cuda:{DEV}")
+
+
+@pytest.mark.parametrize("n", [1, 7, 8, 13, 4096 + 5, (1 << 20) + 3, 32 << 20])
+def test_fill_matches_synth(n):
+    b = _buf(n)
+    ppc.fill_payload(b, n, seed=42, step=1, boundary=2, direction=1, mb=7)
+    assert np.array_equal(_host(b)[:n], P.payload_bytes(42, 1, 2, 1, 7, n))
+
+
+def _pair(**kw):
+    cfg = ppc.make_config(pp=kw.pop("pp", 2), **kw)
+    return ppc.virtual_stages(cfg, DEV)
+
+
+@pytest.mark.parametrize("K", [1, 2, 3])
+@pytest.mark.parametrize("sizes", [[0, 1, 100, 65536, 3 * 65536 + 17, (5 << 20) + 3, 4096]])
+def test_send_recv_bit_exact(K, sizes):
+    comms = _pair(max_msg_bytes=8 << 20, ring_slots=K, chunk_bytes=64 << 10)
+    s = torch.cuda.current_stream()
+    for i, n in enumerate(sizes * 2):              # more messages than slots: ring wraps
+        for d, (snd, rcv) in ((ppc.FWD, (0, 1)), (ppc.BWD, (1, 0))):
+            src = _buf(n)
+            ppc.fill_payload(src, n, seed=42, step=0, boundary=0, direction=d, mb=i)
+            dst = _buf(n)
+            dst.fill_(0xAB)
+            comms[snd].send(d, src, n, mb=i, stream=s)
+            comms[rcv].recv(d, dst, n, mb=i, stream=s)
+            assert np.array_equal(_host(dst)[:n], P.payload_bytes(42, 0, 0, d, i, n)), (i, n, d)
+    for c in comms:
+        assert c.poll() == 0
+        c.disconnect()
+    for c in comms:
+        c.destroy()
+
+
+def test_would_block_and_header_errors():
+    comms = _pair(max_msg_bytes=1 << 20, ring_slots=2, chunk_bytes=64 << 10)
+    s = torch.cuda.current_stream()
+    src, dst = _buf(4096), _buf(4096)
+    assert comms[1].pp_recv(ppc.FWD, dst, 4096, 0, s) == ppc.WOULD_BLOCK   # nothing sent
+    for m in range(2):
+        comms[0].send(ppc.FWD, src, 4096, mb=m, stream=s)
+    assert comms[0].pp_send(ppc.FWD, src, 4096, 2, s) == ppc.WOULD_BLOCK    # both slots full
+    comms[1].recv(ppc.FWD, dst, 4096, mb=0, stream=s)
+    comms[1].recv(ppc.FWD, dst, 2048, mb=1, stream=s)                        # wrong size
+    torch.cuda.synchronize()
+    assert ppc.STATUS[comms[1].poll()] == "SIZE_MISMATCH"
+    assert comms[1].pp_recv(ppc.FWD, dst, 4096, 2, s) == ppc.STATUS.index("STATE")   # poisoned
+    for c in comms:
+        c.disconnect()
+    for c in comms:
+        c.destroy()
+    comms = _pair(max_msg_bytes=1 << 20)
+    comms[0].send(ppc.FWD, src, 4096, mb=3, stream=s)
+    comms[1].recv(ppc.FWD, dst, 4096, mb=4, stream=s)                         # wrong mb
+    torch.cuda.synchronize()
+    assert ppc.STATUS[comms[1].poll()] == "ORDER"
+    for c in comms:
+        c.disconnect()
+    for c in comms:
+        c.destroy()
+
+
+def _masks(n):
+    cache = {}
+
+    def mask(s, d, m):
+        if (s, d, m) not in cache:
+            cache[(s, d, m)] = P.proxy_mask(42, 0, s, d, m, n)
+        return cache[(s, d, m)]
+    return mask
+
+
+def _xor_step(S, M, n, K=2, chunk=64 << 10, engine=ppc.ENGINE_SM, trace=0):
+    cfg = ppc.make_config(pp=S, max_msg_bytes=max(n, 1), ring_slots=K, chunk_bytes=chunk,
+                          engine=engine, trace=trace, channels=2 if engine else 1)
+    comms = ppc.virtual_stages(cfg, DEV)
+    X = [_buf(n) for _ in range(M)]
+    G = [_buf(n) for _ in range(M)]
+    Y = [_buf(n) for _ in range(M)]
+    DX = [_buf(n) for _ in range(M)]
+    for m in range(M):
+        ppc.fill_payload(X[m], n, 42, 0, P.SRC_BOUNDARY, 0, m)
+        ppc.fill_payload(G[m], n, 42, 0, P.SRC_BOUNDARY, 1, m)
+    ctx = [(ppc.XorCtx(42, 0, s, 0), ppc.XorCtx(42, 0, s, 1)) for s in range(S)]
+    args = [ppc.StepArgs(M, n, n, fwd=ppc.STAGE_XOR, bwd=ppc.STAGE_XOR, fwd_user=ctx[s][0],
+                         bwd_user=ctx[s][1], x=X if s == 0 else None, g=G if s == S - 1 else None,
+                         y=Y if s == S - 1 else None, dx=DX if s == 0 else None)
+            for s in range(S)]
+    streams = [torch.cuda.Stream() for _ in range(S)]
+    ppc.step_1f1b_local(comms, args, streams)
+    torch.cuda.synchronize()
+    return comms, Y, DX
+
+
+@pytest.mark.parametrize("S,M", [(2, 1), (2, 4), (3, 4), (4, 8), (5, 3)])
+@pytest.mark.parametrize("engine", [ppc.ENGINE_SM, ppc.ENGINE_CE])
+def test_xor_1f1b_step_matches_oracle(S, M, engine):
+    n = 3 * (64 << 10) + 1234                          # several chunks + ragged tail
+    comms, Y, DX = _xor_step(S, M, n, engine=engine, trace=1)
+    mask = _masks(n)
+    src = lambda m: P.source_activation(42, 0, m, n)
+    dsrc = lambda m: P.source_gradient(42, 0, m, n)
+    Yo, DXo, chans, _ = run_1f1b(S, M, 2, xor_stage(mask, 0), xor_stage(mask, 1), src, dsrc,
+                                 n, n, n)
+    for m in range(M):
+        assert np.array_equal(_host(Y[m])[:n], Yo[m]), m
+        assert np.array_equal(_host(DX[m])[:n], DXo[m]), m
+        y, g = xor_closed_form(S, m, src(m), dsrc(m), mask)
+        assert np.array_equal(Yo[m], y) and np.array_equal(DXo[m], g)
+    # exactly once, in order: every receive record of every stage in ascending seq / mb
+    for c in comms:
+        assert c.poll() == 0
+        recs = [r for r in c.trace() if r["kind"] == 1]
+        for d in (0, 1):
+            rs = [r for r in recs if r["src"] == (c.rank - 1 if d == 0 else c.rank + 1)]
+            assert [r["seq"] for r in rs] == list(range(1, len(rs) + 1))
+            assert [r["mb"] for r in rs] == list(range(len(rs)))
+            assert all(r["t_end_ns"] >= r["t_start_ns"] > 0 for r in rs)
+    for c in comms:
+        c.disconnect()
+    for c in comms:
+        c.destroy()
+
+
+def test_c2_full_size_sampled():
+    """BASELINE configs[1] shape: [1,4096,4096] bf16 boundary (32 MiB), PP=2, M=8, in the
+    launch configuration bench.py times (1 MiB chunks); outputs of micro-batches 0 and 7
+    compared with the oracle closed form byte for byte."""
+    S, M, n = 2, 8, 4096 * 4096 * 2
+    comms, Y, DX = _xor_step(S, M, n, chunk=1 << 20)
+    mask = _masks(n)
+    for m in (0, M - 1):
+        y, g = xor_closed_form(S, m, P.source_activation(42, 0, m, n),
+                               P.source_gradient(42, 0, m, n), mask)
+        assert hashlib.blake2b(_host(Y[m]).tobytes()).digest() == hashlib.blake2b(y.tobytes()).digest()
+        assert np.array_equal(_host(DX[m]), g)
+    for c in comms:
+        c.disconnect()
+    for c in comms:
+        c.destroy()

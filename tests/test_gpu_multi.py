@@ -1,0 +1,39 @@
+"""Multi-GPU parity over NVLink: one process per GPU (torchrun), CUDA-IPC-mapped rings,
+device-side flags/credits.  Skipped when fewer GPUs are visible than a case needs."""
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+PORT = [29611]
+
+
+def _run(case, n, timeout=240):
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    PORT[0] += 1
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(PORT[0]),
+           os.path.join(HERE, "mp_worker.py"), case]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.stdout.count(f"{case} OK") == n
+
+
+@pytest.mark.parametrize("case", ["sendrecv_sm", "sendrecv_ce", "xor_sm", "xor_ce", "timeout"])
+def test_two_gpus(case):
+    _run(case, 2)
+
+
+@pytest.mark.parametrize("case", ["xor_sm", "xor_ce"])
+def test_four_gpu_pipeline(case):
+    _run(case, 4)
+
+
+def test_dcbs_pp2_tp2():
+    _run("dcbs", 4)
