@@ -150,6 +150,11 @@ ppc_status_t ppc_pp_send(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_t byt
 ppc_status_t ppc_pp_recv(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t bytes,
                          long long mb, cudaStream_t s);
 
+/* Enqueue on `s` a (bounded) device wait until the peer has consumed every message sent so
+ * far in direction d, i.e. its credit reached the last send's seq: afterwards the data is
+ * in the receiver's user buffer.  Used to time transfers end to end from the sender. */
+ppc_status_t ppc_pp_wait_consumed(ppc_comm_t* c, ppc_dir_t d, cudaStream_t s);
+
 /* Pure: the 1F1B op list of stage s (of S) over M micro-batches; ops has room for 2M.
  * w = min(S-s-1, M) forwards, then M-w (F, B) pairs, then w backwards. */
 ppc_status_t ppc_schedule_1f1b(int S, int s, int M, ppc_op_t* ops, int* n_ops);

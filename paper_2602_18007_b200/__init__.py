@@ -2,7 +2,7 @@
 
 Every step of the transfer path runs in libppc's sm_100a kernels; this module never
 computes or copies data itself.  If libppc.so is missing this import fails loudly —
-there is no CPU fallback (build with `python -m paper_2602_18007_b200.build` or
+there is no CPU fallback (build with `python paper_2602_18007_b200/build.py` or
 `__graft_entry__.build()`).
 
 Names follow include/ppc.h (pp_send / pp_recv / schedule_1f1b / step_1f1b / DCBS
@@ -22,7 +22,7 @@ LIB_PATH = os.path.join(HERE, "libppc.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with "
-                      "`python -m paper_2602_18007_b200.build` (no CPU fallback exists)")
+                      "`python paper_2602_18007_b200/build.py` (no CPU fallback exists)")
 _lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
 
 # ---- status codes (ppc_status_t) -------------------------------------------------------
@@ -91,6 +91,7 @@ _nccl_id = _sig("ppc_nccl_unique_id", _i, [_vp])
 _group = _sig("ppc_group", _i, [_vp, _i, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)])
 _send = _sig("ppc_pp_send", _i, [_vp, _i, _vp, _sz, _ll, _vp])
 _recv = _sig("ppc_pp_recv", _i, [_vp, _i, _vp, _sz, _ll, _vp])
+_waitc = _sig("ppc_pp_wait_consumed", _i, [_vp, _i, _vp])
 _sched = _sig("ppc_schedule_1f1b", _i, [_i, _i, _i, C.POINTER(Op), C.POINTER(_i)])
 _step = _sig("ppc_step_1f1b", _i, [_vp, C.POINTER(Step), _vp])
 _step_local = _sig("ppc_step_1f1b_local", _i, [C.POINTER(_vp), _i, C.POINTER(Step), C.POINTER(_vp)])
@@ -211,6 +212,9 @@ class Comm:
 
     def recv(self, *a, **k):
         _check(self.pp_recv(*a, **k), "ppc_pp_recv")
+
+    def wait_consumed(self, direction, stream=None):
+        _check(_waitc(self.h, direction, _stream(stream)), "ppc_pp_wait_consumed")
 
     def allreduce(self, g, tensor, nccl_dtype, stream=None):
         p, n = _ptr(tensor)

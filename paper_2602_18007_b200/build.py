@@ -1,6 +1,6 @@
 """Build libppc.so (and the baseline libppcb.so) in-tree for sm_100a with nvcc.
 
-    python -m paper_2602_18007_b200.build          # or __graft_entry__.build()
+    python paper_2602_18007_b200/build.py          # or __graft_entry__.build()
 
 The .so files land next to this file (git-ignored, shipped to the GPU box by gpurun).
 NCCL is the pip 2.28.9 build torch itself loads (site-packages/nvidia/nccl), never the

@@ -360,7 +360,7 @@ ppc_status_t ppc_pp_send(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_t byt
     a.rec_src = c->rank;
     a.rec_dst = h.peer_out;
     a.done = h.push_done;
-    CK(launch_push(a, push_grid(c, n_chunks), s));
+    CK(launch_push(a, push_grid(c, n_chunks), !c->local_mode, s));
   } else {
     CeHeadArgs a{};
     a.hdr = h.o_hdr + slot;
@@ -438,10 +438,29 @@ ppc_status_t ppc_pp_recv(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t bytes, lo
   a.rec_src = h.peer_in;
   a.rec_dst = c->rank;
   if (ppc_status_t ts = time_mark(c, 1, s, true)) return ts;
-  CK(launch_recv(a, recv_grid(c, n_chunks), s));
+  CK(launch_recv(a, recv_grid(c, n_chunks), !c->local_mode, s));
   if (ppc_status_t ts = time_mark(c, 1, s, false)) return ts;
   h.recv_seq = seq;
   if (c->local_mode) CK(cudaEventRecord(h.recvd_ev[slot], s));
+  return PPC_OK;
+}
+
+ppc_status_t ppc_pp_wait_consumed(ppc_comm_t* c, ppc_dir_t d, cudaStream_t s) {
+  ppc_status_t st = check_live(c);
+  if (st) return st;
+  if (d != PPC_FWD && d != PPC_BWD) return PPC_ERR_INVALID_ARG;
+  Chan& h = c->ch[d];
+  if (h.peer_out < 0) return PPC_ERR_NO_NEIGHBOR;
+  if (c->device < 0) return PPC_ERR_STATE;
+  if (h.send_seq == 0) return PPC_OK;
+  DeviceGuard g(c->device);
+  if (c->local_mode) {
+    Chan& rh = h.out_comm->ch[d];
+    if (rh.recv_seq < h.send_seq) return PPC_ERR_WOULD_BLOCK;
+    CK(cudaStreamWaitEvent(s, rh.recvd_ev[h.send_seq % c->K], 0));
+    return PPC_OK;
+  }
+  CK(launch_wait_credit(h.credit, h.send_seq, c->err_dev, c->timeout_ns, s));
   return PPC_OK;
 }
 

@@ -32,6 +32,28 @@ __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
 __device__ __forceinline__ void fence_acq_rel_sys() {
   asm volatile("fence.acq_rel.sys;" ::: "memory");
 }
+// Scope-templated variants: kSys = peer GPU over NVLink (.sys); !kSys = virtual stages on
+// one GPU, where the consumer is on the same device (.gpu is enough and cheaper).
+__device__ __forceinline__ uint64_t ld_acquire_gpu(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+template <bool kSys>
+__device__ __forceinline__ uint64_t ld_acq(const uint64_t* p) {
+  return kSys ? ld_acquire_sys(p) : ld_acquire_gpu(p);
+}
+template <bool kSys>
+__device__ __forceinline__ void st_rel(uint64_t* p, uint64_t v) {
+  if (kSys) st_release_sys(p, v); else st_release_gpu(p, v);
+}
+template <bool kSys>
+__device__ __forceinline__ void fence_rel() {
+  if (kSys) fence_acq_rel_sys(); else asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
 // streaming read of data nobody writes during the kernel (user source buffer)
 __device__ __forceinline__ uint4 ld_src(const uint4* p) {
   uint4 r;
@@ -62,13 +84,14 @@ __device__ __forceinline__ void latch(ErrWord* e, unsigned code, uint64_t seq, u
 }
 
 // Wait until *p >= target (wrap-safe); false on timeout.
+template <bool kSys = true>
 __device__ __forceinline__ bool wait_geq(const uint64_t* p, uint64_t target, uint64_t deadline) {
-  uint64_t v = ld_acquire_sys(p);
+  uint64_t v = ld_acq<kSys>(p);
   int spins = 0;
   while ((int64_t)(v - target) < 0) {
     if (((++spins) & 63) == 0 && globaltimer() > deadline) return false;
     __nanosleep(32);
-    v = ld_acquire_sys(p);
+    v = ld_acq<kSys>(p);
   }
   return true;
 }
@@ -109,6 +132,7 @@ __device__ __forceinline__ void cta_copy(uint8_t* __restrict__ dst, const uint8_
 }
 
 // ---------------------------------------------------------------- K9: push (SM engine)
+template <bool kSys>
 __global__ void __launch_bounds__(kThreads) push_kernel(PushArgs a) {
   uint64_t deadline = 0;
   int fail = 0;
@@ -117,7 +141,7 @@ __global__ void __launch_bounds__(kThreads) push_kernel(PushArgs a) {
     deadline = t0 + a.timeout_ns;
     if (a.rec && blockIdx.x == 0)
       fill_record(a.rec, (long long)t0, a.rec_src, a.rec_dst, a.dir, 0, a.seq, a.mb, a.bytes);
-    if (a.need_credit && !wait_geq(a.credit, a.need_credit, deadline)) {
+    if (a.need_credit && !wait_geq<kSys>(a.credit, a.need_credit, deadline)) {
       latch(a.err, PPC_ERR_TIMEOUT, a.seq, a.dir);
       fail = 1;
     } else if (blockIdx.x == 0) {
@@ -133,7 +157,7 @@ __global__ void __launch_bounds__(kThreads) push_kernel(PushArgs a) {
       uint4* hd = reinterpret_cast<uint4*>(a.hdr);
 #pragma unroll
       for (int j = 0; j < 4; ++j) st_data(hd + j, hs[j]);
-      st_release_sys(a.hdr_flag, a.seq);
+      st_rel<kSys>(a.hdr_flag, a.seq);
     }
   }
   if (__syncthreads_or(fail)) return;
@@ -141,9 +165,9 @@ __global__ void __launch_bounds__(kThreads) push_kernel(PushArgs a) {
     const uint64_t off = (uint64_t)c * a.chunk;
     const uint64_t len = min(a.chunk, a.bytes - off);
     cta_copy<false>(a.dst + off, a.src + off, len);
-    fence_acq_rel_sys();            // every thread: its peer stores before the flag
+    fence_rel<kSys>();              // every thread: its peer stores before the flag
     __syncthreads();
-    if (threadIdx.x == 0) st_release_sys(a.flags + c, a.seq);
+    if (threadIdx.x == 0) st_rel<kSys>(a.flags + c, a.seq);
   }
   if (a.rec) {
     __syncthreads();
@@ -158,6 +182,7 @@ __global__ void __launch_bounds__(kThreads) push_kernel(PushArgs a) {
 }
 
 // ---------------------------------------------------------------- K10: recv + copy-out
+template <bool kSys>
 __global__ void __launch_bounds__(kThreads) recv_kernel(RecvArgs a) {
   uint64_t deadline = 0;
   int fail = 0;
@@ -166,7 +191,7 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(RecvArgs a) {
     deadline = t0 + a.timeout_ns;
     if (a.rec && blockIdx.x == 0)
       fill_record(a.rec, (long long)t0, a.rec_src, a.rec_dst, -1, 1, a.seq, a.mb, a.bytes);
-    if (!wait_geq(a.hdr_flag, a.seq, deadline)) {
+    if (!wait_geq<kSys>(a.hdr_flag, a.seq, deadline)) {
       latch(a.err, PPC_ERR_TIMEOUT, a.seq, 0x100u);
       fail = 1;
     } else {
@@ -183,7 +208,7 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(RecvArgs a) {
   if (__syncthreads_or(fail)) return;
   for (uint32_t c = blockIdx.x; c < a.n_chunks; c += gridDim.x) {
     int f = 0;
-    if (threadIdx.x == 0 && !wait_geq(a.flags + c, a.seq, deadline)) {
+    if (threadIdx.x == 0 && !wait_geq<kSys>(a.flags + c, a.seq, deadline)) {
       latch(a.err, PPC_ERR_TIMEOUT, a.seq, 0x100u | c << 12);
       f = 1;
     }
@@ -198,7 +223,7 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(RecvArgs a) {
     if (atomicAdd(a.done, 1u) == gridDim.x - 1) {
       *a.done = 0;                 // next use of this slot is stream-ordered after us
       __threadfence();
-      st_release_sys(a.peer_credit, a.seq);
+      st_rel<kSys>(a.peer_credit, a.seq);
       if (a.rec) a.rec->t_end_ns = (long long)globaltimer();
     }
   }
@@ -235,12 +260,26 @@ __global__ void ce_flags_kernel(uint64_t* flags, uint32_t c0, uint32_t c1, uint6
   if (rec && threadIdx.x == 0) rec->t_end_ns = (long long)globaltimer();
 }
 
-cudaError_t launch_push(const PushArgs& a, int grid, cudaStream_t s) {
-  push_kernel<<<grid, kThreads, 0, s>>>(a);
+// Wait until the receiver consumed `target` (credit protocol), bounded.
+__global__ void wait_credit_kernel(const uint64_t* credit, uint64_t target, ErrWord* err,
+                                   uint64_t timeout_ns) {
+  if (!wait_geq(credit, target, globaltimer() + timeout_ns)) latch(err, PPC_ERR_TIMEOUT, target, 0x200u);
+}
+
+cudaError_t launch_wait_credit(const uint64_t* credit, uint64_t target, ErrWord* err,
+                               uint64_t timeout_ns, cudaStream_t s) {
+  wait_credit_kernel<<<1, 1, 0, s>>>(credit, target, err, timeout_ns);
   return cudaGetLastError();
 }
-cudaError_t launch_recv(const RecvArgs& a, int grid, cudaStream_t s) {
-  recv_kernel<<<grid, kThreads, 0, s>>>(a);
+
+cudaError_t launch_push(const PushArgs& a, int grid, bool sys, cudaStream_t s) {
+  if (sys) push_kernel<true><<<grid, kThreads, 0, s>>>(a);
+  else push_kernel<false><<<grid, kThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_recv(const RecvArgs& a, int grid, bool sys, cudaStream_t s) {
+  if (sys) recv_kernel<true><<<grid, kThreads, 0, s>>>(a);
+  else recv_kernel<false><<<grid, kThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 cudaError_t launch_ce_head(const CeHeadArgs& a, cudaStream_t s) {
