@@ -41,7 +41,8 @@ def parse():
     ap.add_argument("--seq", type=int, default=4096)
     ap.add_argument("--hidden", type=int, default=4096)
     ap.add_argument("--engine", default="sm", choices=["sm", "ce"])
-    ap.add_argument("--chunk", type=int, default=1 << 20)
+    ap.add_argument("--chunk", type=int, default=0,
+                    help="flag granularity; 0 = 1 MiB across NVLink, 128 KiB for virtual stages")
     ap.add_argument("--channels", type=int, default=1)
     ap.add_argument("--cta", type=int, default=0)
     ap.add_argument("--slots", type=int, default=2)
@@ -199,6 +200,8 @@ def main():
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
+    if not args.chunk:
+        args.chunk = (1 << 20) if distributed else (128 << 10)
     S = args.pp
     nbytes = args.seq * args.hidden * 2
     M = args.M

@@ -304,9 +304,12 @@ def fill_payload(buf, nbytes=None, seed=42, step=0, boundary=0, direction=0, mb=
 
 
 # ---- process wiring (host control plane: bootstrap all-gather) ----------------------
-def virtual_stages(cfg: Config, device: int = 0):
-    """S = cfg.pp virtual stages of one pipeline on one GPU in this process (K11 path)."""
-    comms = [Comm(cfg, cfg.pp, r, device) for r in range(cfg.pp)]
+def virtual_stages(cfg: Config, device=0):
+    """S = cfg.pp virtual stages of one pipeline in this process (K11 path).  `device` is one
+    device index for all stages, or a list with one device per stage (stages on different
+    GPUs of one process: NVLink transfers ordered by events, used for profiling)."""
+    devs = list(device) if isinstance(device, (list, tuple)) else [device] * cfg.pp
+    comms = [Comm(cfg, cfg.pp, r, devs[r]) for r in range(cfg.pp)]
     blobs = [c.export() for c in comms]
     for c in comms:
         c.connect(blobs)

@@ -246,6 +246,16 @@ ppc_status_t ppc_connect(ppc_comm_t* c, const void* all_blobs, size_t blob_bytes
     }
     if (same && cross) return PPC_ERR_INVALID_ARG;
     c->local_mode = same > 0;
+    // virtual stages may also sit on different GPUs of this process (used to profile the
+    // NVLink push without cross-process spins): enable peer access, keep .sys scope
+    c->sys_scope = !c->local_mode;
+    for (int nb : {prev, next}) {
+      if (nb < 0 || !c->local_mode || B[nb].device == c->device) continue;
+      c->sys_scope = true;
+      cudaError_t e = cudaDeviceEnablePeerAccess(B[nb].device, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else CK(e);
+    }
     uint8_t* base_prev = nullptr;
     uint8_t* base_next = nullptr;
     if (prev >= 0) { ppc_status_t st = map_peer(c, B[prev], &base_prev); if (st) return st; }
@@ -360,7 +370,7 @@ ppc_status_t ppc_pp_send(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_t byt
     a.rec_src = c->rank;
     a.rec_dst = h.peer_out;
     a.done = h.push_done;
-    CK(launch_push(a, push_grid(c, n_chunks), !c->local_mode, s));
+    CK(launch_push(a, push_grid(c, n_chunks), c->sys_scope, s));
   } else {
     CeHeadArgs a{};
     a.hdr = h.o_hdr + slot;
@@ -438,7 +448,7 @@ ppc_status_t ppc_pp_recv(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t bytes, lo
   a.rec_src = h.peer_in;
   a.rec_dst = c->rank;
   if (ppc_status_t ts = time_mark(c, 1, s, true)) return ts;
-  CK(launch_recv(a, recv_grid(c, n_chunks), !c->local_mode, s));
+  CK(launch_recv(a, recv_grid(c, n_chunks), c->sys_scope, s));
   if (ppc_status_t ts = time_mark(c, 1, s, false)) return ts;
   h.recv_seq = seq;
   if (c->local_mode) CK(cudaEventRecord(h.recvd_ev[slot], s));

@@ -114,6 +114,7 @@ struct ppc_comm {
   ErrWord* err_host = nullptr;
   ErrWord* err_dev = nullptr;
   bool connected = false, poisoned = false, local_mode = false;
+  bool sys_scope = true;   // a PP neighbour is another GPU: .sys fences, NVLink-sized grids
   Chan ch[2];
   std::vector<void*> opened;          // IPC-opened peer arenas
   ncclComm_t nccl[2] = {nullptr, nullptr};
@@ -175,12 +176,12 @@ inline int push_grid(const ppc_comm* c, uint32_t n_chunks) {
   if (n_chunks == 0) return 1;
   int per = c->cfg.cta_per_channel;
   int chans = std::max(1, c->cfg.channels);
-  int g = per > 0 ? per * chans : (c->local_mode ? 296 : 32 * chans);
+  int g = per > 0 ? per * chans : (c->sys_scope ? 32 * chans : 296);
   return (int)std::max<uint32_t>(1, std::min<uint32_t>(n_chunks, (uint32_t)g));
 }
 inline int recv_grid(const ppc_comm* c, uint32_t n_chunks) {
   if (n_chunks == 0) return 1;
-  int g = c->local_mode ? 296 : 64;
+  int g = c->sys_scope ? 64 : 296;
   return (int)std::max<uint32_t>(1, std::min<uint32_t>(n_chunks, (uint32_t)g));
 }
 

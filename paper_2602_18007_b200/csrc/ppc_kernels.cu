@@ -98,27 +98,63 @@ __device__ __forceinline__ bool wait_geq(const uint64_t* p, uint64_t target, uin
 
 // Copy `len` bytes with the CTA's threads: 16-byte vectors, UNROLL loads in flight per
 // thread before their stores; byte loop for misaligned buffers and the ragged tail.
+// 32-byte vectors (sm_100 LDG/STG.256)
+struct __align__(32) V32 {
+  uint4 lo, hi;
+};
+__device__ __forceinline__ V32 ld_src(const V32* p) {
+  V32 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r.lo.x), "=r"(r.lo.y), "=r"(r.lo.z), "=r"(r.lo.w), "=r"(r.hi.x),
+                 "=r"(r.hi.y), "=r"(r.hi.z), "=r"(r.hi.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ V32 ld_ring(const V32* p) {
+  V32 r;
+  asm volatile("ld.global.cg.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r.lo.x), "=r"(r.lo.y), "=r"(r.lo.z), "=r"(r.lo.w), "=r"(r.hi.x),
+                 "=r"(r.hi.y), "=r"(r.hi.z), "=r"(r.hi.w) : "l"(p) : "memory");
+  return r;
+}
+__device__ __forceinline__ void st_data(V32* p, const V32& v) {
+  asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v.lo.x),
+               "r"(v.lo.y), "r"(v.lo.z), "r"(v.lo.w), "r"(v.hi.x), "r"(v.hi.y), "r"(v.hi.z),
+               "r"(v.hi.w) : "memory");
+}
+
+// Vector body of a CTA copy: VT = uint4 (16 B) or V32 (32 B), U vectors in flight per
+// thread (all loads issued before their stores).
+template <bool kRingSrc, typename VT, int U>
+__device__ __forceinline__ uint64_t cta_copy_body(uint8_t* __restrict__ dst,
+                                                  const uint8_t* __restrict__ src, uint64_t len) {
+  const uint64_t tid = threadIdx.x, nt = blockDim.x;
+  const uint64_t nv = len / sizeof(VT);
+  const VT* s = reinterpret_cast<const VT*>(src);
+  VT* d = reinterpret_cast<VT*>(dst);
+  uint64_t i = tid;
+  for (; i + (U - 1) * nt < nv; i += nt * U) {
+    VT v[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) v[j] = kRingSrc ? ld_ring(s + i + j * nt) : ld_src(s + i + j * nt);
+#pragma unroll
+    for (int j = 0; j < U; ++j) st_data(d + i + j * nt, v[j]);
+  }
+  for (; i < nv; i += nt) st_data(d + i, kRingSrc ? ld_ring(s + i) : ld_src(s + i));
+  return nv * sizeof(VT);
+}
+
 template <bool kRingSrc>
 __device__ __forceinline__ void cta_copy(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src,
                                          uint64_t len) {
-  constexpr int U = 8;
   const uint64_t tid = threadIdx.x, nt = blockDim.x;
   uint64_t body = 0;
-  if ((((uintptr_t)dst | (uintptr_t)src) & 15) == 0) {
-    const uint64_t n16 = len >> 4;
-    const uint4* s = reinterpret_cast<const uint4*>(src);
-    uint4* d = reinterpret_cast<uint4*>(dst);
-    const uint64_t step = nt * U;
-    uint64_t i = tid;
-    for (; i + (U - 1) * nt < n16; i += step) {
-      uint4 v[U];
-#pragma unroll
-      for (int j = 0; j < U; ++j) v[j] = kRingSrc ? ld_ring(s + i + j * nt) : ld_src(s + i + j * nt);
-#pragma unroll
-      for (int j = 0; j < U; ++j) st_data(d + i + j * nt, v[j]);
-    }
-    for (; i < n16; i += nt) st_data(d + i, kRingSrc ? ld_ring(s + i) : ld_src(s + i));
-    body = n16 << 4;
+  const uintptr_t al = (uintptr_t)dst | (uintptr_t)src;
+  if ((al & 31) == 0) {
+    body = cta_copy_body<kRingSrc, V32, 4>(dst, src, len);
+    if (len - body >= 16)
+      body += cta_copy_body<kRingSrc, uint4, 1>(dst + body, src + body, len - body);
+  } else if ((al & 15) == 0) {
+    body = cta_copy_body<kRingSrc, uint4, 8>(dst, src, len);
   }
   for (uint64_t k = body + tid; k < len; k += nt) {
     uint8_t b;

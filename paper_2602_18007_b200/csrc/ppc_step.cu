@@ -58,6 +58,7 @@ struct Stepper {
   const void* send_src = nullptr;
   cudaEvent_t send_free = nullptr;
   bool* send_pending = nullptr;
+  bool direct = false;          // the receive landed in the terminal destination already
 
   ppc_status_t init(ppc_comm* comm, const ppc_step_t* step, cudaStream_t stream) {
     c = comm;
@@ -85,13 +86,19 @@ struct Stepper {
       const bool has_out = kind == 0 ? s < S - 1 : s > 0;
       const int bi = m & 1;
       if (phase == 0) {                                  // input
+        direct = false;
         if (has_in) {
-          uint8_t* r = sb.rbuf[d][bi];
-          if (sb.rpending[d][bi]) CK(cudaStreamWaitEvent(cs, sb.rfree[d][bi], 0));
+          // terminal identity op with a device destination: receive straight into it
+          void* const* dsts = kind == 0 ? st->y : st->dx;
+          void* dst = (!has_out && !(kind == 0 ? st->fwd : st->bwd) && dsts) ? dsts[m] : nullptr;
+          if (dst && is_host_ptr(dst)) dst = nullptr;
+          uint8_t* r = dst ? static_cast<uint8_t*>(dst) : sb.rbuf[d][bi];
+          if (!dst && sb.rpending[d][bi]) CK(cudaStreamWaitEvent(cs, sb.rfree[d][bi], 0));
           ppc_status_t rs = ppc_pp_recv(c, (ppc_dir_t)d, r, bytes, m, cs);
           if (rs == PPC_ERR_WOULD_BLOCK) return PPC_OK;
           if (rs) return rs;
-          sb.rpending[d][bi] = false;
+          if (!dst) sb.rpending[d][bi] = false;
+          direct = dst != nullptr;
           in = r;
         } else {
           const void* const* srcs = kind == 0 ? st->x : st->g;
@@ -147,7 +154,7 @@ struct Stepper {
             void* target = (dst && !host) ? dst : o;
             if (fn(user, m, in, target, in ? bytes : 0, bytes, cs) != 0) return PPC_ERR_INVALID_ARG;
             if (host) CK(cudaMemcpyAsync(dst, o, bytes, cudaMemcpyDeviceToHost, cs));
-          } else if (dst && in && bytes) {
+          } else if (dst && in && bytes && !direct) {
             CK(cudaMemcpyAsync(dst, in, bytes, cudaMemcpyDefault, cs));
           }
         }
