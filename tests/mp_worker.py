@@ -143,6 +143,37 @@ def case_dcbs(rank, world):
     return comm
 
 
+def case_toy(rank, world, bf16=True, steps=5):
+    """C1 toy pipeline across two processes / GPUs; loss vs the oracle (BJ gate 1e-3)."""
+    from paper_2602_18007_b200.toy import ToyStage
+    from oracle import toy as otoy
+    from synth.toy import ROWS, WIDTH, data, init_params
+    M = 4
+    Ws, bs = init_params(42)
+    X, T = data(M, 42)
+    st = ToyStage(rank, ROWS, WIDTH, M, 10.0, bf16, rank, Ws[2 * rank:2 * rank + 2],
+                  bs[2 * rank:2 * rank + 2], X if rank == 0 else T)
+    cfg = ppc.make_config(pp=2, max_msg_bytes=st.boundary_bytes, chunk_bytes=64 << 10)
+    comm = ppc.connect_distributed(cfg, rank, world, rank, with_nccl=False)
+    s = torch.cuda.current_stream()
+    args = st.step_args()
+    losses = []
+    for _ in range(steps):
+        ppc.step_1f1b(comm, args, s)
+        if rank == 1:
+            losses.append(st.loss(s))
+        st.step_end(s)
+    torch.cuda.synchronize()
+    assert comm.poll() == 0
+    if rank == 1:
+        ref, _, _ = otoy.train(Ws, bs, X, T, steps, lr=10.0, dtype=np.float64, bf16=bf16)
+        rel = max(abs(g - r) / abs(r) for g, r in zip(losses, ref))
+        assert rel <= 1e-3, (losses, ref)
+        print(f"toy losses {losses} oracle {ref} max rel {rel:.2e}", flush=True)
+    st.destroy()
+    return comm
+
+
 def main():
     case = sys.argv[1]
     rank = int(os.environ["RANK"])
@@ -159,6 +190,8 @@ def main():
         comm = case_xor(rank, world, ppc.ENGINE_CE)
     elif case == "timeout":
         comm = case_timeout(rank, world)
+    elif case == "toy":
+        comm = case_toy(rank, world)
     elif case == "dcbs":
         comm = case_dcbs(rank, world)
     else:

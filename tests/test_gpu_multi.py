@@ -25,7 +25,7 @@ def _run(case, n, timeout=240):
     assert r.stdout.count(f"{case} OK") == n
 
 
-@pytest.mark.parametrize("case", ["sendrecv_sm", "sendrecv_ce", "xor_sm", "xor_ce", "timeout"])
+@pytest.mark.parametrize("case", ["sendrecv_sm", "sendrecv_ce", "xor_sm", "xor_ce", "timeout", "toy"])
 def test_two_gpus(case):
     _run(case, 2)
 

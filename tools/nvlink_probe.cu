@@ -1,0 +1,179 @@
+// NVLink data-mover probe (one process, two GPUs with peer access): which way of moving a
+// stage-boundary message GPU0 -> GPU1 is fastest on B200?
+//   store  : SM kernel, local 16/32-byte loads -> peer stores (push; current K9 design)
+//   load   : SM kernel on GPU1, peer loads from GPU0 -> local stores (pull)
+//   tma_st : TMA bulk global(local)->smem->global(peer) per CTA (push)
+//   tma_ld : TMA bulk global(peer)->smem->global(local) per CTA on GPU1 (pull)
+//   ce     : cudaMemcpyPeerAsync
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o nvlink_probe nvlink_probe.cu
+#include <cstdio>
+#include <cstdint>
+#include <cstdlib>
+#include <vector>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { \
+  fprintf(stderr, "%s:%d %s -> %s\n", __FILE__, __LINE__, #x, cudaGetErrorString(e)); exit(1);} } while (0)
+
+struct __align__(32) V32 { uint4 lo, hi; };
+
+__device__ __forceinline__ V32 ld32(const V32* p) {
+  V32 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r.lo.x), "=r"(r.lo.y), "=r"(r.lo.z), "=r"(r.lo.w), "=r"(r.hi.x),
+                 "=r"(r.hi.y), "=r"(r.hi.z), "=r"(r.hi.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ V32 ld32_cg(const V32* p) {
+  V32 r;
+  asm volatile("ld.global.cg.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r.lo.x), "=r"(r.lo.y), "=r"(r.lo.z), "=r"(r.lo.w), "=r"(r.hi.x),
+                 "=r"(r.hi.y), "=r"(r.hi.z), "=r"(r.hi.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st32(V32* p, const V32& v) {
+  asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v.lo.x),
+               "r"(v.lo.y), "r"(v.lo.z), "r"(v.lo.w), "r"(v.hi.x), "r"(v.hi.y), "r"(v.hi.z),
+               "r"(v.hi.w) : "memory");
+}
+
+// contiguous per-CTA ranges, U vectors in flight per thread
+template <int U, bool PEER_SRC>
+__global__ void __launch_bounds__(512) simt_copy(V32* dst, const V32* src, size_t nv) {
+  const size_t per = (nv + gridDim.x - 1) / gridDim.x;
+  const size_t b = blockIdx.x * per, e = min(nv, b + per);
+  size_t i = b + threadIdx.x;
+  const size_t nt = blockDim.x;
+  for (; i + (U - 1) * nt < e; i += nt * U) {
+    V32 v[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) v[j] = PEER_SRC ? ld32_cg(src + i + j * nt) : ld32(src + i + j * nt);
+#pragma unroll
+    for (int j = 0; j < U; ++j) st32(dst + i + j * nt, v[j]);
+  }
+  for (; i < e; i += nt) st32(dst + i, PEER_SRC ? ld32_cg(src + i) : ld32(src + i));
+}
+
+// ---- TMA bulk pipeline: one elected thread per CTA, S stages of T bytes in shared memory
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* m, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* m, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(m)), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void tma_load(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* m) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(m)) : "memory");
+}
+__device__ __forceinline__ void tma_store(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+               ::"l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void tma_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void tma_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+template <int S>
+__global__ void tma_copy(uint8_t* dst, const uint8_t* src, size_t bytes, uint32_t tile) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  __shared__ __align__(8) uint64_t mbar[S];
+  if (threadIdx.x != 0) return;
+  const size_t ntiles = (bytes + tile - 1) / tile;
+  const size_t per = (ntiles + gridDim.x - 1) / gridDim.x;
+  const size_t t0 = blockIdx.x * per, t1 = min(ntiles, t0 + per);
+  if (t0 >= t1) return;
+  for (int s = 0; s < S; ++s) mbar_init(&mbar[s], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  const size_t n = t1 - t0;
+  auto len_of = [&](size_t t) { return (uint32_t)min((size_t)tile, bytes - t * tile); };
+  for (size_t j = 0; j < n && j < S; ++j) {
+    const size_t t = t0 + j;
+    mbar_expect_tx(&mbar[j], len_of(t));
+    tma_load(sm + j * tile, src + t * tile, len_of(t), &mbar[j]);
+  }
+  for (size_t i = 0; i < n; ++i) {
+    const int s = i % S;
+    const size_t t = t0 + i;
+    mbar_wait(&mbar[s], (uint32_t)((i / S) & 1));
+    tma_store(dst + t * tile, sm + s * tile, len_of(t));
+    const size_t j = i + S;
+    if (j < n) {
+      tma_wait_read<0>();   // smem of stage s consumed by the store
+      const size_t tj = t0 + j;
+      mbar_expect_tx(&mbar[s], len_of(tj));
+      tma_load(sm + s * tile, src + tj * tile, len_of(tj), &mbar[s]);
+    }
+  }
+  tma_wait_all();
+}
+
+
+
+int main(int argc, char** argv) {
+  int n = 0;
+  CK(cudaGetDeviceCount(&n));
+  if (n < 2) { printf("{\"error\": \"needs 2 GPUs\"}\n"); return 0; }
+  CK(cudaSetDevice(0)); CK(cudaDeviceEnablePeerAccess(1, 0));
+  CK(cudaSetDevice(1)); CK(cudaDeviceEnablePeerAccess(0, 0));
+  const size_t sizes[] = {32ull << 20, 256ull << 20, 1ull << 30};
+  const size_t maxb = 1ull << 30;
+  uint8_t *a0, *b1;
+  CK(cudaSetDevice(0)); CK(cudaMalloc(&a0, maxb)); CK(cudaMemset(a0, 1, maxb));
+  CK(cudaSetDevice(1)); CK(cudaMalloc(&b1, maxb)); CK(cudaMemset(b1, 0, maxb));
+  cudaStream_t s0, s1;
+  CK(cudaSetDevice(0)); CK(cudaStreamCreate(&s0));
+  CK(cudaSetDevice(1)); CK(cudaStreamCreate(&s1));
+  const int tile = 32 << 10, S = 6;
+  for (int d = 0; d < 2; ++d) {
+    CK(cudaSetDevice(d));
+    CK(cudaFuncSetAttribute(tma_copy<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, S * tile));
+  }
+  const int grids[] = {16, 32, 64, 96, 128, 148, 296};
+  for (size_t bytes : sizes) {
+    const int reps = bytes <= (32u << 20) ? 50 : 10;
+    auto run = [&](const char* name, int dev, cudaStream_t st, int grid, auto launch) {
+      CK(cudaSetDevice(dev));
+      cudaEvent_t e0, e1;
+      CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
+      launch();
+      CK(cudaStreamSynchronize(st));
+      CK(cudaEventRecord(e0, st));
+      for (int r = 0; r < reps; ++r) launch();
+      CK(cudaEventRecord(e1, st));
+      CK(cudaEventSynchronize(e1));
+      CK(cudaGetLastError());
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      const double us = ms * 1e3 / reps;
+      printf("{\"mover\": \"%s\", \"bytes\": %zu, \"grid\": %d, \"us\": %.2f, \"gbps\": %.1f}\n", name,
+             bytes, grid, us, bytes / (us * 1e-6) / 1e9);
+      fflush(stdout);
+      cudaEventDestroy(e0); cudaEventDestroy(e1);
+    };
+    const size_t nv = bytes / 32;
+    for (int g : grids) {
+      run("simt_store_u4", 0, s0, g, [&] { simt_copy<4, false><<<g, 512, 0, s0>>>((V32*)b1, (const V32*)a0, nv); });
+      run("simt_store_u8", 0, s0, g, [&] { simt_copy<8, false><<<g, 512, 0, s0>>>((V32*)b1, (const V32*)a0, nv); });
+      run("simt_load_u4", 1, s1, g, [&] { simt_copy<4, true><<<g, 512, 0, s1>>>((V32*)b1, (const V32*)a0, nv); });
+      run("simt_load_u8", 1, s1, g, [&] { simt_copy<8, true><<<g, 512, 0, s1>>>((V32*)b1, (const V32*)a0, nv); });
+      run("tma_store", 0, s0, g, [&] { tma_copy<S><<<g, 32, S * tile, s0>>>(b1, a0, bytes, tile); });
+      run("tma_load", 1, s1, g, [&] { tma_copy<S><<<g, 32, S * tile, s1>>>(b1, a0, bytes, tile); });
+    }
+    run("ce_memcpy_peer", 0, s0, 0, [&] { CK(cudaMemcpyPeerAsync(b1, 1, a0, 0, bytes, s0)); });
+  }
+  return 0;
+}
