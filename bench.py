@@ -40,7 +40,7 @@ def parse():
     ap.add_argument("--M", type=int, default=8)
     ap.add_argument("--seq", type=int, default=4096)
     ap.add_argument("--hidden", type=int, default=4096)
-    ap.add_argument("--engine", default="sm", choices=["sm", "ce"])
+    ap.add_argument("--engine", default="sm", choices=["sm", "ce", "pull"])
     ap.add_argument("--chunk", type=int, default=0,
                     help="flag granularity; 0 = 1 MiB across NVLink, 128 KiB for virtual stages")
     ap.add_argument("--channels", type=int, default=1)
@@ -205,7 +205,7 @@ def main():
     S = args.pp
     nbytes = args.seq * args.hidden * 2
     M = args.M
-    engine = ppc.ENGINE_CE if args.engine == "ce" else ppc.ENGINE_SM
+    engine = {"sm": ppc.ENGINE_SM, "ce": ppc.ENGINE_CE, "pull": ppc.ENGINE_PULL}[args.engine]
     cfg = ppc.make_config(tp=1, pp=S, dp=max(1, world // S) if distributed else 1,
                           max_msg_bytes=nbytes, ring_slots=args.slots, channels=args.channels,
                           chunk_bytes=args.chunk, engine=engine, cta_per_channel=args.cta,

@@ -34,6 +34,7 @@ def parse():
     ap.add_argument("--sizes", default="64K,256K,1M,4M,16M,28M,32M,64M,128M,256M,512M,1G")
     ap.add_argument("--sm", default="16:1M,32:1M,64:1M,32:256K,64:256K,128:256K,32:4M")
     ap.add_argument("--ce", default="1,2,4,8")
+    ap.add_argument("--pull", default="", help="PULL engine specs cta:chunk, e.g. 32:1M,64:1M")
     ap.add_argument("--modes", default="uni,bidir")
     ap.add_argument("--comparators", default="nccl,ce_copy,gloo")
     ap.add_argument("--reps", type=int, default=5)
@@ -199,6 +200,17 @@ def main():
         comm = ppc.connect_distributed(cfg, rank, world, torch.cuda.current_device(),
                                        with_nccl=False)
         bench_ppc(comm, rank, sizes, modes, f"ppc_ce_ch{ch}", a.reps, fh)
+        dist.barrier()
+        comm.disconnect()
+        dist.barrier()
+        comm.destroy()
+    for spec in [x for x in a.pull.split(",") if x]:
+        cta, chunk = spec.split(":")
+        cfg = ppc.make_config(pp=world, max_msg_bytes=maxn, chunk_bytes=size_of(chunk),
+                              cta_per_channel=int(cta), engine=ppc.ENGINE_PULL)
+        comm = ppc.connect_distributed(cfg, rank, world, torch.cuda.current_device(),
+                                       with_nccl=False)
+        bench_ppc(comm, rank, sizes, modes, f"ppc_pull_cta{cta}_chunk{chunk}", a.reps, fh)
         dist.barrier()
         comm.disconnect()
         dist.barrier()

@@ -58,7 +58,16 @@ typedef enum {
 } ppc_status_t;
 
 typedef enum { PPC_FWD = 0, PPC_BWD = 1 } ppc_dir_t;     /* FWD: s -> s+1 ; BWD: s+1 -> s */
-typedef enum { PPC_ENGINE_SM = 0, PPC_ENGINE_CE = 1 } ppc_engine_t;
+/* Data movers (the MPDT analogue):
+ *  SM   : the sender's CTAs load the user buffer and STORE it into the receiver's ring
+ *         over NVLink; the receiver copies the slot out (chunk-pipelined).
+ *  CE   : the sender's copy engines (cudaMemcpyAsync on `channels` streams) write the
+ *         receiver's ring; zero SMs for the data.
+ *  PULL : the sender copies the user buffer into its OWN ring (local HBM) and releases
+ *         per-chunk flags in the receiver's memory; the receiver's CTAs LOAD each chunk over
+ *         NVLink straight into its user buffer (no copy-out; peer loads outrun peer stores
+ *         on B200, see profiles/). */
+typedef enum { PPC_ENGINE_SM = 0, PPC_ENGINE_CE = 1, PPC_ENGINE_PULL = 2 } ppc_engine_t;
 typedef enum { PPC_GROUP_TP = 0, PPC_GROUP_DP = 1, PPC_GROUP_PP = 2 } ppc_group_t;
 typedef enum { PPC_BACKEND_NCCL = 0, PPC_BACKEND_PEER = 1, PPC_BACKEND_NONE = 2 } ppc_backend_t;
 

@@ -31,7 +31,7 @@ STATUS = ["OK", "INVALID_ARG", "GRID_MISMATCH", "RANK_OUT_OF_RANGE", "SELF_SEND"
           "WOULD_BLOCK"]
 OK, WOULD_BLOCK = 0, 14
 FWD, BWD = 0, 1
-ENGINE_SM, ENGINE_CE = 0, 1
+ENGINE_SM, ENGINE_CE, ENGINE_PULL = 0, 1, 2
 GROUP_TP, GROUP_DP, GROUP_PP = 0, 1, 2
 BACKEND_NCCL, BACKEND_PEER, BACKEND_NONE = 0, 1, 2
 BLOB_BYTES = 512

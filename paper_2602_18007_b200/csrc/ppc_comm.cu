@@ -94,7 +94,8 @@ ppc_status_t ppc_create(const ppc_config_t* cfg, int world, int rank, int cuda_d
   if (rank < 0 || rank >= world) return PPC_ERR_RANK_OUT_OF_RANGE;
   if (cfg->ring_slots < 0 || cfg->ring_slots > kMaxSlots || cfg->channels < 0 ||
       cfg->channels > 8 || cfg->cta_per_channel < 0 || cfg->cta_per_channel > 1024 ||
-      (cfg->engine != PPC_ENGINE_SM && cfg->engine != PPC_ENGINE_CE) ||
+      (cfg->engine != PPC_ENGINE_SM && cfg->engine != PPC_ENGINE_CE &&
+       cfg->engine != PPC_ENGINE_PULL) ||
       (cfg->chunk_bytes % 4096) != 0 || cfg->max_msg_bytes == 0 ||
       cfg->max_msg_bytes > (1ull << 40))
     return PPC_ERR_INVALID_ARG;
@@ -268,14 +269,15 @@ ppc_status_t ppc_connect(ppc_comm_t* c, const void* all_blobs, size_t blob_bytes
       h.credit = (uint64_t*)(c->arena + L.credit[d]);
       h.push_done = (uint32_t*)(c->arena + L.push_done[d]);
       if (h.peer_out >= 0) {
-        h.o_payload = ob + L.payload[d];
+        // PULL: the ring slot of an outgoing message lives in the SENDER's arena
+        h.o_payload = (c->cfg.engine == PPC_ENGINE_PULL ? c->arena : ob) + L.payload[d];
         h.o_hdr = (SlotHeader*)(ob + L.hdr[d]);
         h.o_hdr_flag = (uint64_t*)(ob + L.hdr_flag[d]);
         h.o_flags = (uint64_t*)(ob + L.flags[d]);
         if (c->local_mode) h.out_comm = (ppc_comm*)(uintptr_t)B[h.peer_out].comm_ptr;
       }
       if (h.peer_in >= 0) {
-        h.i_payload = c->arena + L.payload[d];
+        h.i_payload = (c->cfg.engine == PPC_ENGINE_PULL ? ib : c->arena) + L.payload[d];
         h.i_hdr = (SlotHeader*)(c->arena + L.hdr[d]);
         h.i_hdr_flag = (uint64_t*)(c->arena + L.hdr_flag[d]);
         h.i_flags = (uint64_t*)(c->arena + L.flags[d]);
@@ -347,7 +349,7 @@ ppc_status_t ppc_pp_send(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_t byt
   uint8_t* dst = h.o_payload + (size_t)slot * c->lay.stride;
   uint64_t* flags = h.o_flags + (size_t)slot * std::max<uint32_t>(c->lay.max_chunks, 1);
   if (ppc_status_t ts = time_mark(c, 0, s, true)) return ts;
-  if (c->cfg.engine == PPC_ENGINE_SM || bytes == 0) {
+  if (c->cfg.engine != PPC_ENGINE_CE || bytes == 0) {     // SM push, or PULL's local staging
     PushArgs a{};
     a.src = static_cast<const uint8_t*>(buf);
     a.dst = dst;

@@ -177,11 +177,14 @@ inline int push_grid(const ppc_comm* c, uint32_t n_chunks) {
   int per = c->cfg.cta_per_channel;
   int chans = std::max(1, c->cfg.channels);
   int g = per > 0 ? per * chans : (c->sys_scope ? 32 * chans : 296);
+  if (c->cfg.engine == PPC_ENGINE_PULL && c->sys_scope && per == 0) g = 64;   // local staging
   return (int)std::max<uint32_t>(1, std::min<uint32_t>(n_chunks, (uint32_t)g));
 }
 inline int recv_grid(const ppc_comm* c, uint32_t n_chunks) {
   if (n_chunks == 0) return 1;
   int g = c->sys_scope ? 64 : 296;
+  if (c->cfg.engine == PPC_ENGINE_PULL && c->sys_scope && c->cfg.cta_per_channel > 0)
+    g = c->cfg.cta_per_channel * std::max(1, c->cfg.channels);      // the pulling CTAs
   return (int)std::max<uint32_t>(1, std::min<uint32_t>(n_chunks, (uint32_t)g));
 }
 

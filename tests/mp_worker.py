@@ -188,6 +188,10 @@ def main():
         comm = case_xor(rank, world, ppc.ENGINE_SM)
     elif case == "xor_ce":
         comm = case_xor(rank, world, ppc.ENGINE_CE)
+    elif case == "xor_pull":
+        comm = case_xor(rank, world, ppc.ENGINE_PULL)
+    elif case == "sendrecv_pull":
+        comm = case_sendrecv(rank, world, ppc.ENGINE_PULL)
     elif case == "timeout":
         comm = case_timeout(rank, world)
     elif case == "toy":

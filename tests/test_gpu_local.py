@@ -120,7 +120,7 @@ def _xor_step(S, M, n, K=2, chunk=64 << 10, engine=ppc.ENGINE_SM, trace=0):
 
 
 @pytest.mark.parametrize("S,M", [(2, 1), (2, 4), (3, 4), (4, 8), (5, 3)])
-@pytest.mark.parametrize("engine", [ppc.ENGINE_SM, ppc.ENGINE_CE])
+@pytest.mark.parametrize("engine", [ppc.ENGINE_SM, ppc.ENGINE_CE, ppc.ENGINE_PULL])
 def test_xor_1f1b_step_matches_oracle(S, M, engine):
     n = 3 * (64 << 10) + 1234                          # several chunks + ragged tail
     comms, Y, DX = _xor_step(S, M, n, engine=engine, trace=1)

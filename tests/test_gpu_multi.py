@@ -25,12 +25,13 @@ def _run(case, n, timeout=240):
     assert r.stdout.count(f"{case} OK") == n
 
 
-@pytest.mark.parametrize("case", ["sendrecv_sm", "sendrecv_ce", "xor_sm", "xor_ce", "timeout", "toy"])
+@pytest.mark.parametrize("case", ["sendrecv_sm", "sendrecv_ce", "sendrecv_pull", "xor_sm", "xor_ce", "xor_pull",
+                                  "timeout", "toy"])
 def test_two_gpus(case):
     _run(case, 2)
 
 
-@pytest.mark.parametrize("case", ["xor_sm", "xor_ce"])
+@pytest.mark.parametrize("case", ["xor_sm", "xor_ce", "xor_pull"])
 def test_four_gpu_pipeline(case):
     _run(case, 4)
 

@@ -32,7 +32,7 @@ ap.add_argument("--channels", type=int, default=1)
 a = ap.parse_args()
 n = size_of(a.size)
 cfg = ppc.make_config(pp=2, max_msg_bytes=n, chunk_bytes=size_of(a.chunk), cta_per_channel=a.cta,
-                      engine=ppc.ENGINE_CE if a.engine == "ce" else ppc.ENGINE_SM,
+                      engine={"sm": ppc.ENGINE_SM, "ce": ppc.ENGINE_CE, "pull": ppc.ENGINE_PULL}[a.engine],
                       channels=a.channels, trace=2)
 comms = ppc.virtual_stages(cfg, [0, 1])
 src = [torch.empty(n, dtype=torch.uint8, device=f"cuda:{d}") for d in (0, 1)]
