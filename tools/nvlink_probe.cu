@@ -54,6 +54,33 @@ __global__ void __launch_bounds__(512) simt_copy(V32* dst, const V32* src, size_
   for (; i < e; i += nt) st32(dst + i, PEER_SRC ? ld32_cg(src + i) : ld32(src + i));
 }
 
+// The K9 push pattern: chunk per CTA iteration, then fence + flag (fence by all threads or
+// by thread 0 only after the barrier), to isolate the cost of the release protocol.
+template <int U, bool ALL_FENCE>
+__global__ void __launch_bounds__(512) simt_store_flagged(V32* dst, const V32* src, size_t nv,
+                                                          size_t chunk_v, uint64_t* flags, uint64_t seq) {
+  const size_t nchunks = (nv + chunk_v - 1) / chunk_v;
+  const size_t nt = blockDim.x;
+  for (size_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const size_t b = c * chunk_v, e = min(nv, b + chunk_v);
+    size_t i = b + threadIdx.x;
+    for (; i + (U - 1) * nt < e; i += nt * U) {
+      V32 v[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) v[j] = ld32(src + i + j * nt);
+#pragma unroll
+      for (int j = 0; j < U; ++j) st32(dst + i + j * nt, v[j]);
+    }
+    for (; i < e; i += nt) st32(dst + i, ld32(src + i));
+    if (ALL_FENCE) asm volatile("fence.acq_rel.sys;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (!ALL_FENCE) asm volatile("fence.acq_rel.sys;" ::: "memory");
+      asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(flags + c), "l"(seq) : "memory");
+    }
+  }
+}
+
 // ---- TMA bulk pipeline: one elected thread per CTA, S stages of T bytes in shared memory
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -165,7 +192,18 @@ int main(int argc, char** argv) {
       cudaEventDestroy(e0); cudaEventDestroy(e1);
     };
     const size_t nv = bytes / 32;
+    uint64_t* flags1;
+    CK(cudaSetDevice(1));
+    CK(cudaMalloc(&flags1, 1 << 16));
     for (int g : grids) {
+      for (size_t ch : {256ull << 10, 1ull << 20}) {
+        const size_t cv = ch / 32;
+        char n1[64], n2[64];
+        snprintf(n1, 64, "flag_allfence_c%zuK", ch >> 10);
+        snprintf(n2, 64, "flag_fence1_c%zuK", ch >> 10);
+        run(n1, 0, s0, g, [&] { simt_store_flagged<4, true><<<g, 512, 0, s0>>>((V32*)b1, (const V32*)a0, nv, cv, flags1, 1); });
+        run(n2, 0, s0, g, [&] { simt_store_flagged<4, false><<<g, 512, 0, s0>>>((V32*)b1, (const V32*)a0, nv, cv, flags1, 1); });
+      }
       run("simt_store_u4", 0, s0, g, [&] { simt_copy<4, false><<<g, 512, 0, s0>>>((V32*)b1, (const V32*)a0, nv); });
       run("simt_store_u8", 0, s0, g, [&] { simt_copy<8, false><<<g, 512, 0, s0>>>((V32*)b1, (const V32*)a0, nv); });
       run("simt_load_u4", 1, s1, g, [&] { simt_copy<4, true><<<g, 512, 0, s1>>>((V32*)b1, (const V32*)a0, nv); });
