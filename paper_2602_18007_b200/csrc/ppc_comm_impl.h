@@ -172,19 +172,27 @@ inline ppc_status_t check_live(ppc_comm* c) {
   return PPC_OK;
 }
 
+inline int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+// Send-side grid: SM push / PULL staging CTAs (MPDT channels x CTAs per channel).
 inline int push_grid(const ppc_comm* c, uint32_t n_chunks) {
   if (n_chunks == 0) return 1;
   int per = c->cfg.cta_per_channel;
   int chans = std::max(1, c->cfg.channels);
-  int g = per > 0 ? per * chans : (c->sys_scope ? 32 * chans : 296);
-  if (c->cfg.engine == PPC_ENGINE_PULL && c->sys_scope && per == 0) g = 64;   // local staging
+  int g = per > 0 ? per * chans : (c->sys_scope ? 64 * chans : 296);
+  if (c->cfg.engine == PPC_ENGINE_PULL && c->sys_scope)
+    g = env_int("PPC_STAGE_CTAS", 128);          // local staging copy: HBM-bound, wide
   return (int)std::max<uint32_t>(1, std::min<uint32_t>(n_chunks, (uint32_t)g));
 }
+// Receive-side grid: copy-out CTAs (SM/CE) or pulling CTAs (PULL).
 inline int recv_grid(const ppc_comm* c, uint32_t n_chunks) {
   if (n_chunks == 0) return 1;
   int g = c->sys_scope ? 64 : 296;
   if (c->cfg.engine == PPC_ENGINE_PULL && c->sys_scope && c->cfg.cta_per_channel > 0)
     g = c->cfg.cta_per_channel * std::max(1, c->cfg.channels);      // the pulling CTAs
+  g = env_int("PPC_RECV_CTAS", g);
   return (int)std::max<uint32_t>(1, std::min<uint32_t>(n_chunks, (uint32_t)g));
 }
 

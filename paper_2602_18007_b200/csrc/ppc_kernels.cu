@@ -201,9 +201,14 @@ __global__ void __launch_bounds__(kThreads) push_kernel(PushArgs a) {
     const uint64_t off = (uint64_t)c * a.chunk;
     const uint64_t len = min(a.chunk, a.bytes - off);
     cta_copy<false>(a.dst + off, a.src + off, len);
-    fence_rel<kSys>();              // every thread: its peer stores before the flag
+    // bar.sync orders every thread's stores before thread 0's release; the release
+    // (fence.acq_rel + strong store, cumulative) publishes them to the peer.  One fence per
+    // CTA-chunk instead of one per thread (profiles/r1_probe: +6-15% at 32 MiB).
     __syncthreads();
-    if (threadIdx.x == 0) st_rel<kSys>(a.flags + c, a.seq);
+    if (threadIdx.x == 0) {
+      fence_rel<kSys>();
+      st_rel<kSys>(a.flags + c, a.seq);
+    }
   }
   if (a.rec) {
     __syncthreads();
