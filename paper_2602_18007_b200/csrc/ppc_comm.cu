@@ -372,7 +372,7 @@ ppc_status_t ppc_pp_send(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_t byt
     a.rec_src = c->rank;
     a.rec_dst = h.peer_out;
     a.done = h.push_done;
-    CK(launch_push(a, push_grid(c, n_chunks), c->sys_scope, s));
+    CK(launch_push(a, push_grid(c, n_chunks), c->sys_scope, env_int("PPC_PUSH_WS", 1) != 0, s));
   } else {
     CeHeadArgs a{};
     a.hdr = h.o_hdr + slot;

@@ -126,8 +126,8 @@ __device__ __forceinline__ void st_data(V32* p, const V32& v) {
 // thread (all loads issued before their stores).
 template <bool kRingSrc, typename VT, int U>
 __device__ __forceinline__ uint64_t cta_copy_body(uint8_t* __restrict__ dst,
-                                                  const uint8_t* __restrict__ src, uint64_t len) {
-  const uint64_t tid = threadIdx.x, nt = blockDim.x;
+                                                  const uint8_t* __restrict__ src, uint64_t len,
+                                                  uint64_t tid, uint64_t nt) {
   const uint64_t nv = len / sizeof(VT);
   const VT* s = reinterpret_cast<const VT*>(src);
   VT* d = reinterpret_cast<VT*>(dst);
@@ -145,16 +145,16 @@ __device__ __forceinline__ uint64_t cta_copy_body(uint8_t* __restrict__ dst,
 
 template <bool kRingSrc>
 __device__ __forceinline__ void cta_copy(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src,
-                                         uint64_t len) {
-  const uint64_t tid = threadIdx.x, nt = blockDim.x;
+                                         uint64_t len, uint64_t tid = threadIdx.x,
+                                         uint64_t nt = blockDim.x) {
   uint64_t body = 0;
   const uintptr_t al = (uintptr_t)dst | (uintptr_t)src;
   if ((al & 31) == 0) {
-    body = cta_copy_body<kRingSrc, V32, 4>(dst, src, len);
+    body = cta_copy_body<kRingSrc, V32, 4>(dst, src, len, tid, nt);
     if (len - body >= 16)
-      body += cta_copy_body<kRingSrc, uint4, 1>(dst + body, src + body, len - body);
+      body += cta_copy_body<kRingSrc, uint4, 1>(dst + body, src + body, len - body, tid, nt);
   } else if ((al & 15) == 0) {
-    body = cta_copy_body<kRingSrc, uint4, 8>(dst, src, len);
+    body = cta_copy_body<kRingSrc, uint4, 8>(dst, src, len, tid, nt);
   }
   for (uint64_t k = body + tid; k < len; k += nt) {
     uint8_t b;
@@ -208,6 +208,104 @@ __global__ void __launch_bounds__(kThreads) push_kernel(PushArgs a) {
     if (threadIdx.x == 0) {
       fence_rel<kSys>();
       st_rel<kSys>(a.flags + c, a.seq);
+    }
+  }
+  if (a.rec) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(a.done, 1u) == gridDim.x - 1) {
+        *a.done = 0;
+        a.rec->t_end_ns = (long long)globaltimer();
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K9': warp-specialised push
+// Warp 0 signals, warps 1..16 copy.  Copy warps stream chunk after chunk and hand each
+// finished chunk to the signal warp through a ring of shared-memory mbarriers (arrive =
+// release.cta); the signal warp waits (acquire.cta), issues the system-scope release fence
+// and the flag store for that chunk while the copy warps are already moving the next one.
+// So the NVLink round trip of the release fence is off the copy path and chunks can be
+// small (receiver copy-out pipelines behind them) without paying a CTA-wide stall per chunk.
+constexpr int kWsCopyWarps = 16;
+constexpr int kWsThreads = 32 * (kWsCopyWarps + 1);
+constexpr int kWsRing = 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* m, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* m) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(m)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(m)), "r"(parity) : "memory");
+}
+
+template <bool kSys>
+__global__ void __launch_bounds__(kWsThreads) push_ws_kernel(PushArgs a) {
+  __shared__ __align__(8) uint64_t full[kWsRing], empty[kWsRing];
+  uint64_t deadline = 0;
+  int fail = 0;
+  if (threadIdx.x == 0) {
+    const uint64_t t0 = globaltimer();
+    deadline = t0 + a.timeout_ns;
+    if (a.rec && blockIdx.x == 0)
+      fill_record(a.rec, (long long)t0, a.rec_src, a.rec_dst, a.dir, 0, a.seq, a.mb, a.bytes);
+    for (int b = 0; b < kWsRing; ++b) {
+      mbar_init(&full[b], kWsCopyWarps);
+      mbar_init(&empty[b], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (a.need_credit && !wait_geq<kSys>(a.credit, a.need_credit, deadline)) {
+      latch(a.err, PPC_ERR_TIMEOUT, a.seq, a.dir);
+      fail = 1;
+    } else if (blockIdx.x == 0) {
+      SlotHeader h = {};
+      h.magic = kMagic;
+      h.dir = (uint8_t)a.dir;
+      h.boundary = (uint8_t)a.boundary;
+      h.bytes = a.bytes;
+      h.seq = a.seq;
+      h.mb = a.mb;
+      h.step = a.step;
+      const uint4* hs = reinterpret_cast<const uint4*>(&h);
+      uint4* hd = reinterpret_cast<uint4*>(a.hdr);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) st_data(hd + j, hs[j]);
+      st_rel<kSys>(a.hdr_flag, a.seq);
+    }
+  }
+  if (__syncthreads_or(fail)) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t i = 0;
+  if (warp == 0) {                                   // signal warp
+    if (lane == 0) {
+      for (uint32_t c = blockIdx.x; c < a.n_chunks; c += gridDim.x, ++i) {
+        const int b = i % kWsRing;
+        mbar_wait(&full[b], (i / kWsRing) & 1);
+        fence_rel<kSys>();
+        st_rel<kSys>(a.flags + c, a.seq);
+        mbar_arrive(&empty[b]);
+      }
+    }
+  } else {                                           // copy warps
+    const uint64_t tid = threadIdx.x - 32, nt = 32 * kWsCopyWarps;
+    for (uint32_t c = blockIdx.x; c < a.n_chunks; c += gridDim.x, ++i) {
+      const int b = i % kWsRing;
+      if (i >= kWsRing) mbar_wait(&empty[b], ((i / kWsRing) - 1) & 1);
+      const uint64_t off = (uint64_t)c * a.chunk;
+      const uint64_t len = min(a.chunk, a.bytes - off);
+      cta_copy<false>(a.dst + off, a.src + off, len, tid, nt);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[b]);
     }
   }
   if (a.rec) {
@@ -313,9 +411,14 @@ cudaError_t launch_wait_credit(const uint64_t* credit, uint64_t target, ErrWord*
   return cudaGetLastError();
 }
 
-cudaError_t launch_push(const PushArgs& a, int grid, bool sys, cudaStream_t s) {
-  if (sys) push_kernel<true><<<grid, kThreads, 0, s>>>(a);
-  else push_kernel<false><<<grid, kThreads, 0, s>>>(a);
+cudaError_t launch_push(const PushArgs& a, int grid, bool sys, bool ws, cudaStream_t s) {
+  if (ws) {
+    if (sys) push_ws_kernel<true><<<grid, kWsThreads, 0, s>>>(a);
+    else push_ws_kernel<false><<<grid, kWsThreads, 0, s>>>(a);
+  } else {
+    if (sys) push_kernel<true><<<grid, kThreads, 0, s>>>(a);
+    else push_kernel<false><<<grid, kThreads, 0, s>>>(a);
+  }
   return cudaGetLastError();
 }
 cudaError_t launch_recv(const RecvArgs& a, int grid, bool sys, cudaStream_t s) {
