@@ -22,23 +22,6 @@ using namespace ppc;
 
 namespace {
 
-// cfg.trace bit 1: record the event opening (begin) / closing (!begin) a timed launch
-ppc_status_t time_mark(ppc_comm* c, int kind, cudaStream_t s, bool begin) {
-  if (!(c->cfg.trace & 2)) return PPC_OK;
-  std::vector<cudaEvent_t>& v = c->tev[kind];
-  size_t& n = c->tev_n[kind];
-  if (begin && n + 2 > 2 * 4096) return PPC_OK;        // list full: stop timing
-  if (!begin && (n & 1) == 0) return PPC_OK;           // begin was skipped
-  if (n == v.size()) {
-    cudaEvent_t e;
-    CK(cudaEventCreate(&e));
-    v.push_back(e);
-  }
-  CK(cudaEventRecord(v[n], s));
-  ++n;
-  return PPC_OK;
-}
-
 ppc_record_t* next_record(ppc_comm* c) {
   // the kernel that stamps the times also writes the record's metadata
   if (!c->cfg.trace || !c->trace_dev || c->trace_n >= kTraceCap) return nullptr;

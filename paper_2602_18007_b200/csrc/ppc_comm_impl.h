@@ -96,6 +96,11 @@ struct StepBufs {
   uint8_t* hbuf[2][2] = {};     // [dir][i] staging for host inputs / outputs
   cudaEvent_t rfree[2][2] = {}, ofree[2][2] = {}, ready = nullptr, join[2] = {};
   bool rpending[2][2] = {}, opending[2][2] = {};
+  // direct (single-copy) mode of same-GPU virtual stages: [dir][i] of the buffer handed to
+  // the receiving stage; held = posted, receiver has not enqueued its copy yet;
+  // cwait = copy enqueued, wait `cons` before overwriting
+  cudaEvent_t dready[2][2] = {}, cons_r[2][2] = {}, cons_o[2][2] = {};
+  bool held_r[2][2] = {}, held_o[2][2] = {}, cwait_r[2][2] = {}, cwait_o[2][2] = {};
 };
 
 }  // namespace ppc_impl
@@ -169,6 +174,23 @@ inline ppc_status_t check_live(ppc_comm* c) {
     c->poisoned = true;
     return PPC_ERR_STATE;
   }
+  return PPC_OK;
+}
+
+// cfg.trace bit 1: record the event opening (begin) / closing (!begin) a timed launch
+inline ppc_status_t time_mark(ppc_comm* c, int kind, cudaStream_t s, bool begin) {
+  if (!(c->cfg.trace & 2)) return PPC_OK;
+  std::vector<cudaEvent_t>& v = c->tev[kind];
+  size_t& n = c->tev_n[kind];
+  if (begin && n + 2 > 2 * 4096) return PPC_OK;        // list full: stop timing
+  if (!begin && (n & 1) == 0) return PPC_OK;           // begin was skipped
+  if (n == v.size()) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    v.push_back(e);
+  }
+  CK(cudaEventRecord(v[n], s));
+  ++n;
   return PPC_OK;
 }
 

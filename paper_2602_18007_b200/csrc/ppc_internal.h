@@ -97,6 +97,9 @@ __device__ __forceinline__ void fill_record(ppc_record_t* r, long long t0, int s
 }
 
 cudaError_t launch_push(const PushArgs& a, int grid, bool sys, bool ws, cudaStream_t s);
+// Same-GPU single copy (direct mode of virtual stages): dst <- src, `bytes`, CTA chunks.
+cudaError_t launch_copy(void* dst, const void* src, uint64_t bytes, uint64_t chunk, int grid,
+                        cudaStream_t s);
 cudaError_t launch_wait_credit(const uint64_t* credit, uint64_t target, ErrWord* err,
                                uint64_t timeout_ns, cudaStream_t s);
 cudaError_t launch_recv(const RecvArgs& a, int grid, bool sys, cudaStream_t s);

@@ -405,6 +405,23 @@ __global__ void wait_credit_kernel(const uint64_t* credit, uint64_t target, ErrW
   if (!wait_geq(credit, target, globaltimer() + timeout_ns)) latch(err, PPC_ERR_TIMEOUT, target, 0x200u);
 }
 
+__global__ void __launch_bounds__(kThreads) copy_kernel(uint8_t* dst, const uint8_t* src,
+                                                        uint64_t bytes, uint64_t chunk) {
+  const uint64_t n = (bytes + chunk - 1) / chunk;
+  for (uint64_t c = blockIdx.x; c < n; c += gridDim.x) {
+    const uint64_t off = c * chunk;
+    cta_copy<false>(dst + off, src + off, min(chunk, bytes - off));
+  }
+}
+
+cudaError_t launch_copy(void* dst, const void* src, uint64_t bytes, uint64_t chunk, int grid,
+                        cudaStream_t s) {
+  if (bytes == 0) return cudaSuccess;
+  copy_kernel<<<grid, kThreads, 0, s>>>(static_cast<uint8_t*>(dst),
+                                        static_cast<const uint8_t*>(src), bytes, chunk);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_wait_credit(const uint64_t* credit, uint64_t target, ErrWord* err,
                                uint64_t timeout_ns, cudaStream_t s) {
   wait_credit_kernel<<<1, 1, 0, s>>>(credit, target, err, timeout_ns);

@@ -3,6 +3,14 @@
 // run on the caller's stream; sends run on the comm's per-direction side streams so that
 // a middle stage's FWD and BWD transfers overlap each other and the next op (the full-
 // duplex NVLink steady state).  Buffer reuse across streams is ordered by events.
+//
+// Direct mode (virtual stages sharing one GPU): the driver sees every stage,
+// so a message is handed over as (pointer, ready event) and the receiving stage makes the
+// ONE copy into its destination; the sending stage's buffer is held until that copy is
+// enqueued and reused only after it completes.  One HBM copy per message instead of the
+// ring's two (push into the slot + copy-out).  PPC_LOCAL_DIRECT=0 selects the ring path.
+#include <deque>
+
 #include "ppc_comm_impl.h"
 
 namespace {
@@ -25,6 +33,9 @@ ppc_status_t ensure_bufs(ppc_comm* c, size_t bytes) {
       for (int i = 0; i < 2; ++i) {
         CK(cudaEventCreateWithFlags(&sb.rfree[d][i], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&sb.ofree[d][i], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&sb.dready[d][i], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&sb.cons_r[d][i], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&sb.cons_o[d][i], cudaEventDisableTiming));
       }
     }
   }
@@ -44,8 +55,20 @@ ppc_status_t ensure_bufs(ppc_comm* c, size_t bytes) {
   return PPC_OK;
 }
 
+// A message handed from one virtual stage to the next in direct mode.
+struct Pending {
+  const void* src;
+  size_t bytes;
+  long long mb;
+  cudaEvent_t ready;      // src is complete once this fires
+  cudaEvent_t consumed;   // recorded by the receiver after its copy (nullptr: user buffer)
+  bool* held;
+  bool* cwait;
+};
+using Mailbox = std::deque<Pending>;
+
 // Resumable enqueuer of one stage's step.  advance() enqueues ops until done or until a
-// virtual-stage send/recv reports PPC_ERR_WOULD_BLOCK (then the caller retries later).
+// virtual-stage send/recv cannot proceed yet (then the caller retries later).
 struct Stepper {
   ppc_comm* c = nullptr;
   const ppc_step_t* st = nullptr;
@@ -58,7 +81,12 @@ struct Stepper {
   const void* send_src = nullptr;
   cudaEvent_t send_free = nullptr;
   bool* send_pending = nullptr;
+  int send_buf = 0;             // direct mode: 0 = user buffer, 1 = rbuf, 2 = obuf
   bool direct = false;          // the receive landed in the terminal destination already
+  // direct mode: inbox[d] = messages sent to this stage in direction d; out[d] = receiver's
+  Mailbox* inbox[2] = {nullptr, nullptr};
+  Mailbox* outbox[2] = {nullptr, nullptr};
+  bool dmode = false;
 
   ppc_status_t init(ppc_comm* comm, const ppc_step_t* step, cudaStream_t stream) {
     c = comm;
@@ -77,6 +105,21 @@ struct Stepper {
 
   bool done() const { return i == ops.size(); }
 
+  // direct mode: may the stage overwrite its buffer (kind 1 = rbuf, 2 = obuf) [d][bi]?
+  // false = the receiving stage has not enqueued its copy yet (caller returns, retries).
+  bool reuse_ok(int kind, int d, int bi, ppc_status_t* err) {
+    StepBufs& sb = c->sb;
+    bool* held = kind == 1 ? &sb.held_r[d][bi] : &sb.held_o[d][bi];
+    bool* cw = kind == 1 ? &sb.cwait_r[d][bi] : &sb.cwait_o[d][bi];
+    if (*held) return false;
+    if (*cw) {
+      cudaEvent_t e = kind == 1 ? sb.cons_r[d][bi] : sb.cons_o[d][bi];
+      if (cudaStreamWaitEvent(cs, e, 0) != cudaSuccess) { *err = PPC_ERR_CUDA; return false; }
+      *cw = false;
+    }
+    return true;
+  }
+
   ppc_status_t advance(bool* progressed) {
     StepBufs& sb = c->sb;
     while (i < ops.size()) {
@@ -93,11 +136,31 @@ struct Stepper {
           void* dst = (!has_out && !(kind == 0 ? st->fwd : st->bwd) && dsts) ? dsts[m] : nullptr;
           if (dst && is_host_ptr(dst)) dst = nullptr;
           uint8_t* r = dst ? static_cast<uint8_t*>(dst) : sb.rbuf[d][bi];
-          if (!dst && sb.rpending[d][bi]) CK(cudaStreamWaitEvent(cs, sb.rfree[d][bi], 0));
-          ppc_status_t rs = ppc_pp_recv(c, (ppc_dir_t)d, r, bytes, m, cs);
-          if (rs == PPC_ERR_WOULD_BLOCK) return PPC_OK;
-          if (rs) return rs;
-          if (!dst) sb.rpending[d][bi] = false;
+          if (dmode) {
+            Mailbox& box = *inbox[d];
+            if (box.empty()) return PPC_OK;                       // sender not there yet
+            ppc_status_t e = PPC_OK;
+            if (!dst && !reuse_ok(1, d, bi, &e)) return e;
+            Pending p = box.front();
+            if (p.bytes != bytes) return PPC_ERR_SIZE_MISMATCH;
+            if (p.mb != m) return PPC_ERR_ORDER;
+            box.pop_front();
+            CK(cudaStreamWaitEvent(cs, p.ready, 0));
+            if (ppc_status_t ts = time_mark(c, 0, cs, true)) return ts;
+            CK(launch_copy(r, p.src, bytes, c->chunk, recv_grid(c, (uint32_t)((bytes + c->chunk - 1) / c->chunk)), cs));
+            if (ppc_status_t ts = time_mark(c, 0, cs, false)) return ts;
+            if (p.consumed) {
+              CK(cudaEventRecord(p.consumed, cs));
+              *p.held = false;
+              *p.cwait = true;
+            }
+          } else {
+            if (!dst && sb.rpending[d][bi]) CK(cudaStreamWaitEvent(cs, sb.rfree[d][bi], 0));
+            ppc_status_t rs = ppc_pp_recv(c, (ppc_dir_t)d, r, bytes, m, cs);
+            if (rs == PPC_ERR_WOULD_BLOCK) return PPC_OK;
+            if (rs) return rs;
+            if (!dst) sb.rpending[d][bi] = false;
+          }
           direct = dst != nullptr;
           in = r;
         } else {
@@ -105,7 +168,12 @@ struct Stepper {
           in = srcs ? srcs[m] : nullptr;
           if (in && is_host_ptr(in)) {
             uint8_t* r = sb.rbuf[d][bi];
-            if (sb.rpending[d][bi]) CK(cudaStreamWaitEvent(cs, sb.rfree[d][bi], 0));
+            if (dmode) {
+              ppc_status_t e = PPC_OK;
+              if (!reuse_ok(1, d, bi, &e)) return e;
+            } else if (sb.rpending[d][bi]) {
+              CK(cudaStreamWaitEvent(cs, sb.rfree[d][bi], 0));
+            }
             sb.rpending[d][bi] = false;
             CK(cudaMemcpyAsync(r, in, bytes, cudaMemcpyHostToDevice, cs));
             in = r;
@@ -118,39 +186,47 @@ struct Stepper {
         ppc_stage_fn fn = kind == 0 ? st->fwd : st->bwd;
         void* user = kind == 0 ? st->fwd_user : st->bwd_user;
         if (has_out) {
-          if (fn) {
+          if (fn || !in) {
+            if (dmode) {
+              ppc_status_t e = PPC_OK;
+              if (!reuse_ok(2, d, bi, &e)) return e;
+            } else if (sb.opending[d][bi]) {
+              CK(cudaStreamWaitEvent(cs, sb.ofree[d][bi], 0));
+            }
             uint8_t* o = sb.obuf[d][bi];
-            if (sb.opending[d][bi]) CK(cudaStreamWaitEvent(cs, sb.ofree[d][bi], 0));
-            if (fn(user, m, in, o, in ? bytes : 0, bytes, cs) != 0) return PPC_ERR_INVALID_ARG;
-            send_src = o;
+            if (fn && fn(user, m, in, o, in ? bytes : 0, bytes, cs) != 0) return PPC_ERR_INVALID_ARG;
+            send_src = o;          // no input and no fn: scratch contents
             send_free = sb.ofree[d][bi];
             send_pending = &sb.opending[d][bi];
+            send_buf = 2;
           } else if (in == sb.rbuf[d][bi]) {
             send_src = in;
             send_free = sb.rfree[d][bi];
             send_pending = &sb.rpending[d][bi];
-          } else if (in) {                               // caller's device buffer
+            send_buf = 1;
+          } else {                                       // caller's device buffer
             send_src = in;
             send_free = nullptr;
             send_pending = nullptr;
-          } else {                                       // no input given: scratch contents
-            send_src = sb.obuf[d][bi];
-            send_free = sb.ofree[d][bi];
-            send_pending = &sb.opending[d][bi];
-            if (sb.opending[d][bi]) CK(cudaStreamWaitEvent(cs, sb.ofree[d][bi], 0));
+            send_buf = 0;
           }
-          CK(cudaEventRecord(sb.ready, cs));
-          CK(cudaStreamWaitEvent(c->side[d], sb.ready, 0));
+          if (!dmode) {
+            CK(cudaEventRecord(sb.ready, cs));
+            CK(cudaStreamWaitEvent(c->side[d], sb.ready, 0));
+          }
         } else {
           void* const* dsts = kind == 0 ? st->y : st->dx;
           void* dst = dsts ? dsts[m] : nullptr;
           if (fn) {
             const bool host = dst && is_host_ptr(dst);
-            uint8_t* o = sb.obuf[d][bi];
-            if (sb.opending[d][bi]) {
+            if (dmode) {
+              ppc_status_t e = PPC_OK;
+              if (!reuse_ok(2, d, bi, &e)) return e;
+            } else if (sb.opending[d][bi]) {
               CK(cudaStreamWaitEvent(cs, sb.ofree[d][bi], 0));
               sb.opending[d][bi] = false;
             }
+            uint8_t* o = sb.obuf[d][bi];
             void* target = (dst && !host) ? dst : o;
             if (fn(user, m, in, target, in ? bytes : 0, bytes, cs) != 0) return PPC_ERR_INVALID_ARG;
             if (host) CK(cudaMemcpyAsync(dst, o, bytes, cudaMemcpyDeviceToHost, cs));
@@ -163,12 +239,30 @@ struct Stepper {
       }
       if (phase == 2) {                                  // send
         if (has_out) {
-          ppc_status_t ss = ppc_pp_send(c, (ppc_dir_t)d, send_src, bytes, m, c->side[d]);
-          if (ss == PPC_ERR_WOULD_BLOCK) return PPC_OK;
-          if (ss) return ss;
-          if (send_free) {
-            CK(cudaEventRecord(send_free, c->side[d]));
-            *send_pending = true;
+          if (dmode) {
+            // hand the buffer to the next stage: it makes the one copy
+            cudaEvent_t rdy = sb.dready[d][bi];
+            CK(cudaEventRecord(rdy, cs));
+            Pending p{send_src, bytes, (long long)m, rdy, nullptr, nullptr, nullptr};
+            if (send_buf == 1) {
+              p.consumed = sb.cons_r[d][bi];
+              p.held = &sb.held_r[d][bi];
+              p.cwait = &sb.cwait_r[d][bi];
+            } else if (send_buf == 2) {
+              p.consumed = sb.cons_o[d][bi];
+              p.held = &sb.held_o[d][bi];
+              p.cwait = &sb.cwait_o[d][bi];
+            }
+            if (p.held) *p.held = true;
+            outbox[d]->push_back(p);
+          } else {
+            ppc_status_t ss = ppc_pp_send(c, (ppc_dir_t)d, send_src, bytes, m, c->side[d]);
+            if (ss == PPC_ERR_WOULD_BLOCK) return PPC_OK;
+            if (ss) return ss;
+            if (send_free) {
+              CK(cudaEventRecord(send_free, c->side[d]));
+              *send_pending = true;
+            }
           }
         }
         *progressed = true;
@@ -180,6 +274,7 @@ struct Stepper {
   }
 
   ppc_status_t finish() {
+    if (dmode) return PPC_OK;
     for (int d = 0; d < 2; ++d) {
       CK(cudaEventRecord(c->sb.join[d], c->side[d]));
       CK(cudaStreamWaitEvent(cs, c->sb.join[d], 0));
@@ -211,14 +306,26 @@ extern "C" ppc_status_t ppc_step_1f1b_local(ppc_comm_t* const* comms, int S,
                                             const cudaStream_t* streams) {
   if (!comms || !steps || !streams || S < 1) return PPC_ERR_INVALID_ARG;
   std::vector<Stepper> sp(S);
+  bool same_device = true;
   for (int k = 0; k < S; ++k) {
     ppc_status_t r = check_live(comms[k]);
     if (r) return r;
     if (comms[k]->cfg.pp != S || comms[k]->pp_i != k) return PPC_ERR_INVALID_ARG;
     if (S > 1 && !comms[k]->local_mode) return PPC_ERR_INVALID_ARG;
     if (steps[k].M != steps[0].M) return PPC_ERR_INVALID_ARG;
+    same_device = same_device && comms[k]->device == comms[0]->device;
     DeviceGuard g(comms[k]->device);
     if ((r = sp[k].init(comms[k], &steps[k], streams[k]))) return r;
+  }
+  // mailboxes of the direct (single-copy) mode: box[k][d] = messages into stage k, dir d
+  std::vector<Mailbox> box(2 * S);
+  const bool dmode = S > 1 && same_device && env_int("PPC_LOCAL_DIRECT", 1) != 0;
+  for (int k = 0; k < S && dmode; ++k) {
+    sp[k].dmode = true;
+    sp[k].inbox[0] = &box[2 * k + 0];
+    sp[k].inbox[1] = &box[2 * k + 1];
+    sp[k].outbox[0] = k + 1 < S ? &box[2 * (k + 1) + 0] : nullptr;
+    sp[k].outbox[1] = k > 0 ? &box[2 * (k - 1) + 1] : nullptr;
   }
   // round-robin: a dependency-respecting enqueue order (every recv after its send)
   for (;;) {

@@ -121,7 +121,13 @@ def _xor_step(S, M, n, K=2, chunk=64 << 10, engine=ppc.ENGINE_SM, trace=0):
 
 @pytest.mark.parametrize("S,M", [(2, 1), (2, 4), (3, 4), (4, 8), (5, 3)])
 @pytest.mark.parametrize("engine", [ppc.ENGINE_SM, ppc.ENGINE_CE, ppc.ENGINE_PULL])
-def test_xor_1f1b_step_matches_oracle(S, M, engine):
+@pytest.mark.parametrize("direct", [0, 1])
+def test_xor_1f1b_step_matches_oracle(S, M, engine, direct, monkeypatch):
+    """direct=0: the ring path (push -> flags -> copy-out); direct=1: the single-copy hand-off
+    of same-GPU virtual stages."""
+    if direct and engine != ppc.ENGINE_SM:
+        pytest.skip("direct mode does not use the engine")
+    monkeypatch.setenv("PPC_LOCAL_DIRECT", str(direct))
     n = 3 * (64 << 10) + 1234                          # several chunks + ragged tail
     comms, Y, DX = _xor_step(S, M, n, engine=engine, trace=1)
     mask = _masks(n)
@@ -137,6 +143,8 @@ def test_xor_1f1b_step_matches_oracle(S, M, engine):
     # exactly once, in order: every receive record of every stage in ascending seq / mb
     for c in comms:
         assert c.poll() == 0
+        if direct:
+            continue
         recs = [r for r in c.trace() if r["kind"] == 1]
         for d in (0, 1):
             rs = [r for r in recs if r["src"] == (c.rank - 1 if d == 0 else c.rank + 1)]
@@ -149,12 +157,15 @@ def test_xor_1f1b_step_matches_oracle(S, M, engine):
         c.destroy()
 
 
-def test_c2_full_size_sampled():
+@pytest.mark.parametrize("direct", [1, 0])
+def test_c2_full_size_sampled(direct, monkeypatch):
     """BASELINE configs[1] shape: [1,4096,4096] bf16 boundary (32 MiB), PP=2, M=8, in the
-    launch configuration bench.py times (1 MiB chunks); outputs of micro-batches 0 and 7
-    compared with the oracle closed form byte for byte."""
+    launch configuration bench.py times at N=1 (128 KiB chunks, direct single-copy hand-off;
+    and the ring path); outputs of micro-batches 0 and 7 compared with the oracle closed
+    form byte for byte."""
+    monkeypatch.setenv("PPC_LOCAL_DIRECT", str(direct))
     S, M, n = 2, 8, 4096 * 4096 * 2
-    comms, Y, DX = _xor_step(S, M, n, chunk=1 << 20)
+    comms, Y, DX = _xor_step(S, M, n, chunk=128 << 10)
     mask = _masks(n)
     for m in (0, M - 1):
         y, g = xor_closed_form(S, m, P.source_activation(42, 0, m, n),
