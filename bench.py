@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--hidden", type=int, default=4096)
     ap.add_argument("--engine", default="sm", choices=["sm", "ce", "pull"])
     ap.add_argument("--chunk", type=int, default=0,
-                    help="flag granularity; 0 = 1 MiB across NVLink, 128 KiB for virtual stages")
+                    help="flag granularity; 0 = 512 KiB across NVLink, 128 KiB for virtual stages")
     ap.add_argument("--channels", type=int, default=1)
     ap.add_argument("--cta", type=int, default=0)
     ap.add_argument("--slots", type=int, default=2)
@@ -201,7 +201,8 @@ def main():
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
     if not args.chunk:
-        args.chunk = (1 << 20) if distributed else (128 << 10)
+        # tuned on 2x B200 (profiles/r1_tune_step_ws.jsonl): 512 KiB chunks x 64 CTAs
+        args.chunk = (512 << 10) if distributed else (128 << 10)
     S = args.pp
     nbytes = args.seq * args.hidden * 2
     M = args.M
@@ -260,32 +261,41 @@ def main():
     for _ in range(args.warmup):
         one_step()
     barrier()
-    for c in comms:
-        c.kernel_times(0), c.kernel_times(1)
 
-    # ---- timed region: K steps, CUDA events on every stage stream, max over ranks
+    def timed_region(instrumented: bool):
+        """K steps between barriers + synchronize; CUDA events on every stage stream;
+        max over ranks.  instrumented: CUDA-event pairs around every transfer launch."""
+        for c in comms:
+            c.set_trace(2 if instrumented else 0)
+            c.kernel_times(0), c.kernel_times(1)
+        ev0 = [torch.cuda.Event(enable_timing=True) for _ in stages]
+        ev1 = [torch.cuda.Event(enable_timing=True) for _ in stages]
+        barrier()
+        for e, st in zip(ev0, streams):
+            e.record(st)
+        for _ in range(args.steps):
+            one_step()
+        for e, st in zip(ev1, streams):
+            e.record(st)
+        barrier()
+        return max_over_ranks(max(a.elapsed_time(b) for a, b in zip(ev0, ev1)))
+
+    # ---- headline timed region (no instrumentation), clocks sampled during it
     sampler = ClockSampler(dev)
-    ev0 = [torch.cuda.Event(enable_timing=True) for _ in stages]
-    ev1 = [torch.cuda.Event(enable_timing=True) for _ in stages]
-    barrier()
     sampler.start()
-    for e, st in zip(ev0, streams):
-        e.record(st)
-    for _ in range(args.steps):
-        one_step()
-    for e, st in zip(ev1, streams):
-        e.record(st)
-    barrier()
+    ms_total = timed_region(False)
     clocks = sampler.stop()
-    ms_total = max(a.elapsed_time(b) for a, b in zip(ev0, ev1))
-    ms_total = max_over_ranks(ms_total)
     ms_step = ms_total / args.steps
     tokens = pipelines * M * args.seq * args.steps
     value = tokens / (ms_total * 1e-3)
+    # ---- the same K steps again with per-launch CUDA events for the kernel roofline
+    ms_instr = timed_region(True)
     push_ms = [t for c in comms for t in c.kernel_times(0)]
     recv_ms = [t for c in comms for t in c.kernel_times(1)]
+    for c in comms:
+        c.set_trace(0)
     n_launch_local = len(push_ms) + len(recv_ms)
-    n_launch = int(max_over_ranks(0) if False else n_launch_local)
+    n_launch = n_launch_local
     if distributed:
         t = torch.tensor([n_launch_local], dtype=torch.float64)
         dist.all_reduce(t)
@@ -305,11 +315,19 @@ def main():
         unit, bound = "GB/s", "hbm"
         peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
     achieved = alg / (avg_push_ms * 1e-3) / 1e9
+    kname = "ppc::push_ws_kernel (SM push over NVLink)" if distributed else \
+        "ppc::copy_kernel (virtual-stage single-copy hand-off)"
     roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
             "frac": achieved / peak, "traffic": ncu_traffic("push_n%d" % min(world, 2)),
-            "kernel": "ppc::push_kernel", "alg_bytes_per_launch": alg,
+            "kernel": kname, "alg_bytes_per_launch": alg,
             "avg_launch_us": avg_push_ms * 1e3, "launches_timed": len(push_ms),
             "peak_source": peak_src,
+            "timed_region": "second pass of the same K steps with per-launch CUDA events "
+                            f"(step {ms_instr / args.steps:.3f} ms instrumented vs {ms_step:.3f} plain)",
+            "step_aggregate": {"bytes_per_step": alg * len(push_ms) / max(1, args.steps),
+                               "achieved": alg * len(push_ms) / (ms_instr * 1e-3) / 1e9,
+                               "note": "this process's transfer launches of the step (both "
+                                       "directions, concurrent) over the instrumented step time"},
             "recv_avg_launch_us": (statistics.mean(recv_ms) * 1e3) if recv_ms else None}
     boundary_gbps = 2 * M * nbytes * pipelines * (S - 1) * args.steps / (ms_total * 1e-3) / 1e9
 

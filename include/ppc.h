@@ -191,6 +191,8 @@ ppc_status_t ppc_trace(ppc_comm_t* c, ppc_record_t* out, int* n);  /* synchroniz
  * last call, from the CUDA-event pairs of cfg.trace bit 1, in launch order; synchronizes
  * the device.  *n in: capacity, out: entries written.  Resets the list. */
 ppc_status_t ppc_kernel_times(ppc_comm_t* c, int kind, float* ms, int* n);
+/* Switch cfg.trace bits at run time (bit 0 only if the comm was created with it). */
+ppc_status_t ppc_set_trace(ppc_comm_t* c, int trace);
 ppc_status_t ppc_disconnect(ppc_comm_t* c);        /* phase 1: close peer handles, NCCL    */
 ppc_status_t ppc_destroy(ppc_comm_t* c);           /* phase 2 (after a caller barrier)     */
 const char* ppc_status_str(ppc_status_t st);

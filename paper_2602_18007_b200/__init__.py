@@ -99,6 +99,7 @@ _allreduce = _sig("ppc_allreduce", _i, [_vp, _i, _vp, _sz, _i, _vp])
 _poll = _sig("ppc_poll", _i, [_vp])
 _trace = _sig("ppc_trace", _i, [_vp, C.POINTER(Record), C.POINTER(_i)])
 _ktimes = _sig("ppc_kernel_times", _i, [_vp, _i, C.POINTER(C.c_float), C.POINTER(_i)])
+_set_trace = _sig("ppc_set_trace", _i, [_vp, _i])
 _disconnect = _sig("ppc_disconnect", _i, [_vp])
 _destroy = _sig("ppc_destroy", _i, [_vp])
 _status_str = _sig("ppc_status_str", C.c_char_p, [_i])
@@ -223,6 +224,9 @@ class Comm:
 
     def poll(self) -> int:
         return _poll(self.h)
+
+    def set_trace(self, trace: int):
+        _check(_set_trace(self.h, trace), "ppc_set_trace")
 
     def kernel_times(self, kind: int, cap=4096):
         """Device ms of each send (0) / recv (1) launch since the last call (cfg.trace & 2)."""

@@ -508,6 +508,13 @@ ppc_status_t ppc_kernel_times(ppc_comm_t* c, int kind, float* ms, int* n) {
   return PPC_OK;
 }
 
+ppc_status_t ppc_set_trace(ppc_comm_t* c, int trace) {
+  if (!c || trace < 0 || trace > 3) return PPC_ERR_INVALID_ARG;
+  if ((trace & 1) && !c->trace_dev) return PPC_ERR_STATE;
+  c->cfg.trace = trace;
+  return PPC_OK;
+}
+
 ppc_status_t ppc_disconnect(ppc_comm_t* c) {
   if (!c) return PPC_ERR_INVALID_ARG;
   DeviceGuard g(c->device);
