@@ -183,6 +183,18 @@ ppc_status_t ppc_step_1f1b_local(ppc_comm_t* const* comms, int S, const ppc_step
 ppc_status_t ppc_allreduce(ppc_comm_t* c, ppc_group_t g, void* buf, size_t count,
                            int nccl_dtype, cudaStream_t s);
 
+/* Heterogeneous-collective composition (§2.2):
+ * in-place sum allreduce over ALL ranks of this rank's tensor-parallel slice (every rank
+ * with the same tp_i), composed as (1) a vendor-CCL (NCCL) allreduce inside each
+ * homogeneous subgroup = this stage's DP group, (2) the cross-subgroup exchange of the
+ * intermediate results between the subgroup leaders (dp_i = 0) over the PP peer path
+ * (libppc send/recv along the stage chain: reduce forward, result backward), (3) an NCCL
+ * broadcast from the leader inside each subgroup.  count * element size <= max_msg_bytes.
+ * nccl_dtype: ncclFloat32 (7), ncclFloat16 (6), ncclBfloat16 (9) or ncclInt32 (2).
+ * One process per GPU only (not virtual stages). */
+ppc_status_t ppc_hetero_allreduce(ppc_comm_t* c, void* buf, size_t count, int nccl_dtype,
+                                  cudaStream_t s);
+
 /* ---- diagnostics and teardown ---------------------------------------------------------- */
 ppc_status_t ppc_poll(ppc_comm_t* c);              /* non-blocking read of the error word  */
 ppc_status_t ppc_trace(ppc_comm_t* c, ppc_record_t* out, int* n);  /* synchronizes the device;

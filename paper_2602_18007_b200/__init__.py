@@ -96,6 +96,7 @@ _sched = _sig("ppc_schedule_1f1b", _i, [_i, _i, _i, C.POINTER(Op), C.POINTER(_i)
 _step = _sig("ppc_step_1f1b", _i, [_vp, C.POINTER(Step), _vp])
 _step_local = _sig("ppc_step_1f1b_local", _i, [C.POINTER(_vp), _i, C.POINTER(Step), C.POINTER(_vp)])
 _allreduce = _sig("ppc_allreduce", _i, [_vp, _i, _vp, _sz, _i, _vp])
+_hx_allreduce = _sig("ppc_hetero_allreduce", _i, [_vp, _vp, _sz, _i, _vp])
 _poll = _sig("ppc_poll", _i, [_vp])
 _trace = _sig("ppc_trace", _i, [_vp, C.POINTER(Record), C.POINTER(_i)])
 _ktimes = _sig("ppc_kernel_times", _i, [_vp, _i, C.POINTER(C.c_float), C.POINTER(_i)])
@@ -221,6 +222,12 @@ class Comm:
         p, n = _ptr(tensor)
         _check(_allreduce(self.h, g, p, tensor.numel(), nccl_dtype, _stream(stream)),
                "ppc_allreduce")
+
+    def hetero_allreduce(self, tensor, nccl_dtype, stream=None):
+        """NCCL inside each stage's DP subgroup + leader exchange over the PP peer path."""
+        p, _ = _ptr(tensor)
+        _check(_hx_allreduce(self.h, p, tensor.numel(), nccl_dtype, _stream(stream)),
+               "ppc_hetero_allreduce")
 
     def poll(self) -> int:
         return _poll(self.h)

@@ -475,6 +475,52 @@ ppc_status_t ppc_allreduce(ppc_comm_t* c, ppc_group_t g, void* buf, size_t count
   return PPC_OK;
 }
 
+ppc_status_t ppc_hetero_allreduce(ppc_comm_t* c, void* buf, size_t count, int nccl_dtype,
+                                  cudaStream_t s) {
+  ppc_status_t st = check_live(c);
+  if (st) return st;
+  if (c->device < 0 || c->local_mode) return PPC_ERR_STATE;
+  int kind, esize;
+  switch (nccl_dtype) {
+    case ncclFloat32: kind = 0; esize = 4; break;
+    case ncclFloat16: kind = 1; esize = 2; break;
+    case ncclBfloat16: kind = 2; esize = 2; break;
+    case ncclInt32: kind = 3; esize = 4; break;
+    default: return PPC_ERR_INVALID_ARG;
+  }
+  if (count == 0) return PPC_OK;
+  if (!buf) return PPC_ERR_INVALID_ARG;
+  const size_t bytes = count * (size_t)esize;
+  if (bytes > c->cfg.max_msg_bytes) return PPC_ERR_TOO_LARGE;
+  DeviceGuard g(c->device);
+  const bool multi_dp = c->members[PPC_GROUP_DP].size() > 1;
+  if (multi_dp && !c->nccl[PPC_GROUP_DP]) return PPC_ERR_STATE;
+  // (1) intra-subgroup aggregation with the vendor CCL
+  if (multi_dp && ncclAllReduce(buf, buf, count, (ncclDataType_t)nccl_dtype, ncclSum,
+                                c->nccl[PPC_GROUP_DP], s) != ncclSuccess)
+    return PPC_ERR_NCCL;
+  // (2) cross-subgroup exchange of the intermediate results between leaders, P2P path
+  const int S = c->cfg.pp, sidx = c->pp_i;
+  const long long tag = 0x7FFFFFFFll;
+  if (c->dp_i == 0 && S > 1) {
+    if (!c->hx_buf) CK(cudaMalloc(&c->hx_buf, c->cfg.max_msg_bytes));
+    if (sidx > 0) {                                   // partial sum of stages < sidx
+      if ((st = ppc_pp_recv(c, PPC_FWD, c->hx_buf, bytes, tag, s))) return st;
+      CK(launch_add(buf, c->hx_buf, count, kind, s));
+    }
+    if (sidx < S - 1) {
+      if ((st = ppc_pp_send(c, PPC_FWD, buf, bytes, tag, s))) return st;
+      if ((st = ppc_pp_recv(c, PPC_BWD, buf, bytes, tag, s))) return st;   // the total
+    }
+    if (sidx > 0 && (st = ppc_pp_send(c, PPC_BWD, buf, bytes, tag, s))) return st;
+  }
+  // (3) intra-subgroup broadcast from the leader (DP rank 0)
+  if (multi_dp && ncclBroadcast(buf, buf, count, (ncclDataType_t)nccl_dtype, 0,
+                                c->nccl[PPC_GROUP_DP], s) != ncclSuccess)
+    return PPC_ERR_NCCL;
+  return PPC_OK;
+}
+
 ppc_status_t ppc_poll(ppc_comm_t* c) {
   if (!c) return PPC_ERR_INVALID_ARG;
   if (!c->err_host) return PPC_OK;
@@ -559,6 +605,7 @@ ppc_status_t ppc_destroy(ppc_comm_t* c) {
     if (c->trace_dev) cudaFree(c->trace_dev);
     for (int k = 0; k < 2; ++k)
       for (cudaEvent_t e : c->tev[k]) cudaEventDestroy(e);
+    if (c->hx_buf) cudaFree(c->hx_buf);
     if (c->arena) cudaFree(c->arena);
     if (c->err_host) cudaFreeHost(c->err_host);
   }

@@ -133,6 +133,7 @@ struct ppc_comm {
   std::vector<cudaEvent_t> tev[2];
   size_t tev_n[2] = {0, 0};
   StepBufs sb;
+  uint8_t* hx_buf = nullptr;      // hetero allreduce receive scratch (max_msg bytes)
   Blob blob{};
 };
 

@@ -97,6 +97,8 @@ __device__ __forceinline__ void fill_record(ppc_record_t* r, long long t0, int s
 }
 
 cudaError_t launch_push(const PushArgs& a, int grid, bool sys, bool ws, cudaStream_t s);
+// dst[i] += src[i] for the hetero allreduce (dtype: 0 f32, 1 f16, 2 bf16, 3 i32).
+cudaError_t launch_add(void* dst, const void* src, size_t count, int dtype, cudaStream_t s);
 // Same-GPU single copy (direct mode of virtual stages): dst <- src, `bytes`, CTA chunks.
 cudaError_t launch_copy(void* dst, const void* src, uint64_t bytes, uint64_t chunk, int grid,
                         cudaStream_t s);

@@ -10,7 +10,10 @@
 //                        sender waits ld.acquire.sys credit >= seq - K before writing a slot.
 // Flags and credits are monotone u64 sequence numbers (never reset); every wait compares
 // wrap-safe and is bounded by %globaltimer (§4.3 P:L211 hangs).
+#include <algorithm>
 #include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include "ppc_internal.h"
 
@@ -403,6 +406,29 @@ __global__ void ce_flags_kernel(uint64_t* flags, uint32_t c0, uint32_t c1, uint6
 __global__ void wait_credit_kernel(const uint64_t* credit, uint64_t target, ErrWord* err,
                                    uint64_t timeout_ns) {
   if (!wait_geq(credit, target, globaltimer() + timeout_ns)) latch(err, PPC_ERR_TIMEOUT, target, 0x200u);
+}
+
+template <typename T>
+__global__ void add_kernel(T* __restrict__ dst, const T* __restrict__ src, size_t n) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = dst[i] + src[i];
+}
+
+cudaError_t launch_add(void* dst, const void* src, size_t count, int dtype, cudaStream_t s) {
+  if (count == 0) return cudaSuccess;
+  const int grid = (int)std::min<size_t>((count + 255) / 256, 148 * 8);
+  switch (dtype) {
+    case 0: add_kernel<float><<<grid, 256, 0, s>>>((float*)dst, (const float*)src, count); break;
+    case 1: add_kernel<__half><<<grid, 256, 0, s>>>((__half*)dst, (const __half*)src, count); break;
+    case 2:
+      add_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((__nv_bfloat16*)dst,
+                                                     (const __nv_bfloat16*)src, count);
+      break;
+    case 3: add_kernel<int32_t><<<grid, 256, 0, s>>>((int32_t*)dst, (const int32_t*)src, count); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
 }
 
 __global__ void __launch_bounds__(kThreads) copy_kernel(uint8_t* dst, const uint8_t* src,

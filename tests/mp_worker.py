@@ -174,6 +174,27 @@ def case_toy(rank, world, bf16=True, steps=5):
     return comm
 
 
+def case_hetero(rank, world):
+    """NEXT-2: hetero allreduce = NCCL in each stage's DP subgroup + leader exchange over the
+    PP path + NCCL broadcast; compared exactly (integer-valued fp32) with the oracle."""
+    from oracle.collectives import allreduce_reference
+    dp = 2 if world >= 4 else 1
+    pp = world // dp
+    cfg = ppc.make_config(tp=1, pp=pp, dp=dp, max_msg_bytes=8 << 20)
+    comm = ppc.connect_distributed(cfg, rank, world, rank, with_nccl=True)
+    n = (1 << 20) + 3
+    idx = np.arange(n, dtype=np.int64)
+    vals = {r: ((r + 1) * (idx % 7 + 1)).astype(np.float32) for r in range(world)}
+    ref = allreduce_reference(vals, list(range(world)))
+    for dtype, torch_dt in ((7, torch.float32), (2, torch.int32)):
+        t = torch.from_numpy(vals[rank]).to(torch_dt).cuda()
+        comm.hetero_allreduce(t, dtype, stream=torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        assert comm.poll() == 0
+        assert np.array_equal(t.cpu().numpy().astype(np.float64), ref), (rank, dtype)
+    return comm
+
+
 def main():
     case = sys.argv[1]
     rank = int(os.environ["RANK"])
@@ -196,6 +217,8 @@ def main():
         comm = case_timeout(rank, world)
     elif case == "toy":
         comm = case_toy(rank, world)
+    elif case == "hetero":
+        comm = case_hetero(rank, world)
     elif case == "dcbs":
         comm = case_dcbs(rank, world)
     else:

@@ -38,3 +38,8 @@ def test_four_gpu_pipeline(case):
 
 def test_dcbs_pp2_tp2():
     _run("dcbs", 4)
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_hetero_allreduce(n):
+    _run("hetero", n)
