@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--channels", type=int, default=1)
     ap.add_argument("--cta", type=int, default=0)
     ap.add_argument("--slots", type=int, default=2)
+    ap.add_argument("--zc", type=int, default=1,
+                    help="N>=2: register the step's send buffers (zero-copy NVLink pulls)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -172,12 +174,14 @@ def run_reference(args):
 
 
 def workload_config(args, pipelines, virtual):
-    return {"workload": f"C2: LLaMA-8B-shaped PP={args.pp} boundary [1,{args.seq},{args.hidden}] "
+    name = "C2: " if (args.pp, args.hidden, args.M) == (2, 4096, 8) else ""
+    model = "Qwen2-7B" if args.hidden == 3584 else "LLaMA-8B"
+    return {"workload": f"{name}{model}-shaped PP={args.pp} boundary [1,{args.seq},{args.hidden}] "
                         f"bf16, M={args.M}, 1F1B comm-only step",
             "pp": args.pp, "pipelines": pipelines, "virtual_stages": virtual, "M": args.M,
             "seq": args.seq, "hidden": args.hidden, "msg_bytes": args.seq * args.hidden * 2,
             "engine": args.engine, "chunk_bytes": args.chunk, "channels": args.channels,
-            "ring_slots": args.slots,
+            "ring_slots": args.slots, "zero_copy_sends": bool(args.zc) and not virtual,
             "l2": "inputs larger than L2 (M x 32 MiB per stage per direction, 256 MiB)"}
 
 
@@ -238,6 +242,9 @@ def main():
     args_dev = [ppc.StepArgs(M, nbytes, nbytes, x=X.get(s), g=G.get(s), y=Y.get(s),
                              dx=DX.get(s)) for s in stages]
     streams = [torch.cuda.Stream() for _ in stages]
+    if distributed and args.zc:
+        # zero-copy: the stage inputs X / G are registered send buffers; receivers pull them
+        ppc.register_tensors(comms[0], [t for s in stages for t in X.get(s, []) + G.get(s, [])])
 
     def one_step(a=None):
         a = a or args_dev

@@ -164,6 +164,20 @@ ppc_status_t ppc_pp_recv(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t bytes,
  * in the receiver's user buffer.  Used to time transfers end to end from the sender. */
 ppc_status_t ppc_pp_wait_consumed(ppc_comm_t* c, ppc_dir_t d, cudaStream_t s);
 
+/* Zero-copy send buffers.  ppc_register(c, ptr, bytes) registers the device allocation that
+ * contains [ptr, ptr+bytes) (one CUDA IPC handle per allocation) and returns a blob of
+ * PPC_REG_BLOB_BYTES; the caller gives every PP neighbour the blob (control plane, e.g. a
+ * gloo all-gather) and the neighbour calls ppc_register_import.  Afterwards ppc_pp_send from
+ * a registered range moves no data on the sender: it publishes (segment, offset) in the
+ * receiver's slot header and the receiver's CTAs LOAD the payload over NVLink straight into
+ * their user buffer (one pass, no ring copy).  The send completes on its stream only when
+ * the receiver has consumed the message (rendezvous), so the buffer may be reused after it.
+ * Blobs of non-neighbours are accepted and ignored.  Up to 256 registrations per comm. */
+#define PPC_REG_BLOB_BYTES 128
+ppc_status_t ppc_register(ppc_comm_t* c, const void* ptr, size_t bytes, void* blob,
+                          size_t* blob_bytes);
+ppc_status_t ppc_register_import(ppc_comm_t* c, const void* blob, size_t blob_bytes);
+
 /* Pure: the 1F1B op list of stage s (of S) over M micro-batches; ops has room for 2M.
  * w = min(S-s-1, M) forwards, then M-w (F, B) pairs, then w backwards. */
 ppc_status_t ppc_schedule_1f1b(int S, int s, int M, ppc_op_t* ops, int* n_ops);

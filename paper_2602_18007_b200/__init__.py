@@ -97,6 +97,9 @@ _step = _sig("ppc_step_1f1b", _i, [_vp, C.POINTER(Step), _vp])
 _step_local = _sig("ppc_step_1f1b_local", _i, [C.POINTER(_vp), _i, C.POINTER(Step), C.POINTER(_vp)])
 _allreduce = _sig("ppc_allreduce", _i, [_vp, _i, _vp, _sz, _i, _vp])
 _hx_allreduce = _sig("ppc_hetero_allreduce", _i, [_vp, _vp, _sz, _i, _vp])
+_register = _sig("ppc_register", _i, [_vp, _vp, _sz, _vp, C.POINTER(_sz)])
+_reg_import = _sig("ppc_register_import", _i, [_vp, _vp, _sz])
+REG_BLOB_BYTES = 128
 _poll = _sig("ppc_poll", _i, [_vp])
 _trace = _sig("ppc_trace", _i, [_vp, C.POINTER(Record), C.POINTER(_i)])
 _ktimes = _sig("ppc_kernel_times", _i, [_vp, _i, C.POINTER(C.c_float), C.POINTER(_i)])
@@ -222,6 +225,18 @@ class Comm:
         p, n = _ptr(tensor)
         _check(_allreduce(self.h, g, p, tensor.numel(), nccl_dtype, _stream(stream)),
                "ppc_allreduce")
+
+    def register(self, buf, nbytes=None) -> bytes:
+        """Register a send buffer for zero-copy pulls; returns the blob for the neighbours."""
+        p, n = _ptr(buf)
+        out = C.create_string_buffer(REG_BLOB_BYTES)
+        sz = C.c_size_t(REG_BLOB_BYTES)
+        _check(_register(self.h, p, n if nbytes is None else nbytes, out, C.byref(sz)),
+               "ppc_register")
+        return out.raw
+
+    def register_import(self, blob: bytes):
+        _check(_reg_import(self.h, blob, len(blob)), "ppc_register_import")
 
     def hetero_allreduce(self, tensor, nccl_dtype, stream=None):
         """NCCL inside each stage's DP subgroup + leader exchange over the PP peer path."""
@@ -350,3 +365,16 @@ def connect_distributed(cfg: Config, rank: int, world: int, device: int, pg=None
         ids = [allids[min(tp_m)].get("tp", zero), allids[min(dp_m)].get("dp", zero)]
     comm.connect(blobs, ids)
     return comm
+
+
+def register_tensors(comm: Comm, tensors, pg=None):
+    """Collective: register this rank's send buffers for zero-copy pulls and import every
+    neighbour's registrations (gloo all-gather of the registration blobs)."""
+    import torch.distributed as dist
+    mine = [comm.register(t) for t in (tensors or [])]
+    world = dist.get_world_size(pg)
+    allb = [None] * world
+    dist.all_gather_object(allb, mine, group=pg)
+    for blobs in allb:
+        for b in blobs:
+            comm.register_import(b)

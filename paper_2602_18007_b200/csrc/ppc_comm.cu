@@ -22,12 +22,58 @@ using namespace ppc;
 
 namespace {
 
+
 ppc_record_t* next_record(ppc_comm* c) {
   // the kernel that stamps the times also writes the record's metadata
   if (!c->cfg.trace || !c->trace_dev || c->trace_n >= kTraceCap) return nullptr;
   return c->trace_dev + c->trace_n++;
 }
 
+struct RegBlob {
+  uint32_t magic;
+  int32_t rank, pid;
+  uint32_t seg;
+  uint64_t base, size, host_hash;
+  cudaIpcMemHandle_t ipc;
+  uint8_t pad[PPC_REG_BLOB_BYTES - 4 * 4 - 8 * 3 - sizeof(cudaIpcMemHandle_t)];
+};
+static_assert(sizeof(RegBlob) == PPC_REG_BLOB_BYTES, "reg blob size");
+constexpr uint32_t kRegMagic = 0x52435050u;   // "PPCR"
+
+// Allocation range of a device pointer (driver API through the runtime's entry point, so
+// libppc does not link libcuda directly).
+bool alloc_range(const void* p, uintptr_t* base, size_t* size) {
+  using Fn = CUresult (*)(void*, CUpointer_attribute, CUdeviceptr);
+  static Fn fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuPointerGetAttribute", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !f)
+      return false;
+    fn = reinterpret_cast<Fn>(f);
+  }
+  CUdeviceptr b = 0;
+  size_t sz = 0;
+  if (fn(&b, CU_POINTER_ATTRIBUTE_RANGE_START_ADDR, (CUdeviceptr)(uintptr_t)p) != CUDA_SUCCESS ||
+      fn(&sz, CU_POINTER_ATTRIBUTE_RANGE_SIZE, (CUdeviceptr)(uintptr_t)p) != CUDA_SUCCESS)
+    return false;
+  *base = (uintptr_t)b;
+  *size = sz;
+  return true;
+}
+
+int find_reg(const ppc_comm* c, const void* p, size_t bytes, uint64_t* off) {
+  const uintptr_t a = (uintptr_t)p;
+  for (size_t i = 0; i < c->regs.size(); ++i) {
+    const auto& r = c->regs[i];
+    if (a >= r.base && a + bytes <= r.base + r.size) {
+      *off = a - r.base;
+      return (int)i;
+    }
+  }
+  return -1;
+}
 }  // namespace
 
 extern "C" {
@@ -332,7 +378,26 @@ ppc_status_t ppc_pp_send(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_t byt
   uint8_t* dst = h.o_payload + (size_t)slot * c->lay.stride;
   uint64_t* flags = h.o_flags + (size_t)slot * std::max<uint32_t>(c->lay.max_chunks, 1);
   if (ppc_status_t ts = time_mark(c, 0, s, true)) return ts;
-  if (c->cfg.engine != PPC_ENGINE_CE || bytes == 0) {     // SM push, or PULL's local staging
+  uint64_t zc_off = 0;
+  const int zc_seg = (!c->local_mode && bytes > 0) ? find_reg(c, buf, bytes, &zc_off) : -1;
+  if (zc_seg >= 0) {              // registered buffer: publish it, the receiver pulls it
+    PublishArgs p{};
+    p.hdr = h.o_hdr + slot;
+    p.hdr_flag = h.o_hdr_flag + slot;
+    p.credit = h.credit;
+    p.need_credit = need;
+    p.bytes = bytes;
+    p.seq = seq;
+    p.src_off = zc_off;
+    p.mb = mb;
+    p.src_seg = (uint32_t)zc_seg;
+    p.dir = d;
+    p.boundary = (uint32_t)boundary;
+    p.err = c->err_dev;
+    p.timeout_ns = c->timeout_ns;
+    CK(launch_publish(p, s));
+    CK(launch_wait_credit(h.credit, seq, c->err_dev, c->timeout_ns, s));   // rendezvous
+  } else if (c->cfg.engine != PPC_ENGINE_CE || bytes == 0) {  // SM push, or PULL's staging
     PushArgs a{};
     a.src = static_cast<const uint8_t*>(buf);
     a.dst = dst;
@@ -432,6 +497,7 @@ ppc_status_t ppc_pp_recv(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t bytes, lo
   a.rec = next_record(c);
   a.rec_src = h.peer_in;
   a.rec_dst = c->rank;
+  a.seg_tab = c->seg_tab ? c->seg_tab + (d == PPC_FWD ? 0 : 1) * kMaxSeg : nullptr;
   if (ppc_status_t ts = time_mark(c, 1, s, true)) return ts;
   CK(launch_recv(a, recv_grid(c, n_chunks), c->sys_scope, s));
   if (ppc_status_t ts = time_mark(c, 1, s, false)) return ts;
@@ -472,6 +538,70 @@ ppc_status_t ppc_allreduce(ppc_comm_t* c, ppc_group_t g, void* buf, size_t count
   if (ncclAllReduce(buf, buf, count, (ncclDataType_t)nccl_dtype, ncclSum, c->nccl[g], s) !=
       ncclSuccess)
     return PPC_ERR_NCCL;
+  return PPC_OK;
+}
+
+
+ppc_status_t ppc_register(ppc_comm_t* c, const void* ptr, size_t bytes, void* blob,
+                          size_t* blob_bytes) {
+  if (!c || !ptr || !blob || !blob_bytes || *blob_bytes < PPC_REG_BLOB_BYTES)
+    return PPC_ERR_INVALID_ARG;
+  if (c->device < 0) return PPC_ERR_STATE;
+  DeviceGuard g(c->device);
+  uintptr_t base = 0;
+  size_t size = 0;
+  if (!alloc_range(ptr, &base, &size) || (uintptr_t)ptr + bytes > base + size)
+    return PPC_ERR_INVALID_ARG;
+  RegBlob rb{};
+  rb.magic = kRegMagic;
+  rb.rank = c->rank;
+  rb.pid = c->blob.pid;
+  rb.host_hash = c->blob.host_hash;
+  rb.base = base;
+  rb.size = size;
+  int seg = -1;
+  for (size_t i = 0; i < c->regs.size(); ++i)
+    if (c->regs[i].base == base) seg = (int)i;
+  if (seg < 0) {
+    if ((int)c->regs.size() >= kMaxSeg) return PPC_ERR_TOO_LARGE;
+    seg = (int)c->regs.size();
+    c->regs.push_back({base, size});
+  }
+  rb.seg = (uint32_t)seg;
+  CK(cudaIpcGetMemHandle(&rb.ipc, (void*)base));
+  memcpy(blob, &rb, sizeof(rb));
+  *blob_bytes = PPC_REG_BLOB_BYTES;
+  return PPC_OK;
+}
+
+ppc_status_t ppc_register_import(ppc_comm_t* c, const void* blob, size_t blob_bytes) {
+  if (!c || !blob || blob_bytes != PPC_REG_BLOB_BYTES) return PPC_ERR_INVALID_ARG;
+  if (!c->connected || c->device < 0) return PPC_ERR_STATE;
+  RegBlob rb;
+  memcpy(&rb, blob, sizeof(rb));
+  if (rb.magic != kRegMagic || rb.seg >= (uint32_t)kMaxSeg) return PPC_ERR_INVALID_ARG;
+  const int side = rb.rank == c->ch[PPC_FWD].peer_in ? 0 : (rb.rank == c->ch[PPC_BWD].peer_in ? 1 : -1);
+  if (side < 0) return PPC_OK;                                   // not a PP neighbour
+  DeviceGuard g(c->device);
+  if (!c->seg_tab) {
+    CK(cudaMalloc(&c->seg_tab, 2 * kMaxSeg * sizeof(uint64_t)));
+    CK(cudaMemset(c->seg_tab, 0, 2 * kMaxSeg * sizeof(uint64_t)));
+  }
+  uint64_t mapped = 0;
+  if (rb.pid == c->blob.pid && rb.host_hash == c->blob.host_hash) {
+    mapped = rb.base;                                            // same process: UVA pointer
+  } else {
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, rb.ipc, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      if (getenv("PPC_DEBUG")) fprintf(stderr, "ppc: reg import %s\n", cudaGetErrorString(e));
+      return PPC_ERR_CUDA;
+    }
+    c->reg_opened.push_back(p);
+    mapped = (uint64_t)(uintptr_t)p;
+  }
+  CK(cudaMemcpy(c->seg_tab + side * kMaxSeg + rb.seg, &mapped, sizeof(mapped),
+                cudaMemcpyHostToDevice));
   return PPC_OK;
 }
 
@@ -567,6 +697,8 @@ ppc_status_t ppc_disconnect(ppc_comm_t* c) {
   if (c->device >= 0) cudaDeviceSynchronize();
   for (int i = 0; i < 2; ++i)
     if (c->nccl[i]) { ncclCommDestroy(c->nccl[i]); c->nccl[i] = nullptr; }
+  for (void* p : c->reg_opened) cudaIpcCloseMemHandle(p);
+  c->reg_opened.clear();
   for (void* p : c->opened) cudaIpcCloseMemHandle(p);
   c->opened.clear();
   for (int d = 0; d < 2; ++d) {
@@ -606,6 +738,7 @@ ppc_status_t ppc_destroy(ppc_comm_t* c) {
     for (int k = 0; k < 2; ++k)
       for (cudaEvent_t e : c->tev[k]) cudaEventDestroy(e);
     if (c->hx_buf) cudaFree(c->hx_buf);
+    if (c->seg_tab) cudaFree(c->seg_tab);
     if (c->arena) cudaFree(c->arena);
     if (c->err_host) cudaFreeHost(c->err_host);
   }

@@ -7,6 +7,7 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <cuda.h>
 #include <nccl.h>
 #include <unistd.h>
 
@@ -134,6 +135,11 @@ struct ppc_comm {
   size_t tev_n[2] = {0, 0};
   StepBufs sb;
   uint8_t* hx_buf = nullptr;      // hetero allreduce receive scratch (max_msg bytes)
+  // zero-copy registrations: mine (index = segment id) and the neighbours' mapped bases
+  struct Reg { uintptr_t base; size_t size; };
+  std::vector<Reg> regs;
+  uint64_t* seg_tab = nullptr;    // device [2][kMaxSeg]: 0 = from prev (FWD in), 1 = next
+  std::vector<void*> reg_opened;
   Blob blob{};
 };
 

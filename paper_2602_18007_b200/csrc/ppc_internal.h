@@ -9,17 +9,23 @@ namespace ppc {
 constexpr uint32_t kMagic = 0x48435043u;     // SPEC.md S:L403 chunk-header magic, reused
 constexpr int kThreads = 512;                // CTA size of the copy kernels
 constexpr int kMaxSlots = 64;
+constexpr int kMaxSeg = 256;                 // registered send buffers per peer
+constexpr uint16_t kHdrZeroCopy = 1;         // header flag: payload is in a registered buffer
 
-// 64-byte slot header, little-endian.
+// 64-byte slot header, little-endian.  Ring path: the payload is in
+// the slot.  Zero-copy path (flags & kHdrZeroCopy): the payload stays in the sender's
+// registered buffer (segment src_seg, offset src_off) and the receiver pulls it.
 struct __align__(64) SlotHeader {
   uint32_t magic;
   uint8_t dir, boundary;
-  uint16_t zero;
+  uint16_t flags;
   uint64_t bytes;
   uint64_t seq;
   int64_t mb;
   uint64_t step;
-  uint8_t pad[24];
+  uint64_t src_off;
+  uint32_t src_seg;
+  uint8_t pad[12];
 };
 static_assert(sizeof(SlotHeader) == 64, "slot header is 64 B");
 
@@ -65,7 +71,22 @@ struct RecvArgs {
   uint64_t timeout_ns;
   ppc_record_t* rec;
   int rec_src, rec_dst;
+  const uint64_t* seg_tab;      // zero-copy: mapped bases of the sender's registered buffers
 };
+
+// Zero-copy publication of a registered send buffer: credit wait, header, header flag.
+struct PublishArgs {
+  SlotHeader* hdr;
+  uint64_t* hdr_flag;
+  const uint64_t* credit;
+  uint64_t need_credit;
+  uint64_t bytes, seq, src_off;
+  int64_t mb;
+  uint32_t src_seg, dir, boundary;
+  ErrWord* err;
+  uint64_t timeout_ns;
+};
+cudaError_t launch_publish(const PublishArgs& a, cudaStream_t s);
 
 // CE engine pieces: header/credit kernel before the copies, flag kernel after each.
 struct CeHeadArgs {

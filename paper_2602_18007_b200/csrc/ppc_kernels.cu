@@ -326,11 +326,13 @@ __global__ void __launch_bounds__(kWsThreads) push_ws_kernel(PushArgs a) {
 // ---------------------------------------------------------------- K10: recv + copy-out
 template <bool kSys>
 __global__ void __launch_bounds__(kThreads) recv_kernel(RecvArgs a) {
+  __shared__ const uint8_t* s_zc_src;   // zero-copy: the sender's buffer, mapped here
   uint64_t deadline = 0;
   int fail = 0;
   if (threadIdx.x == 0) {
     const uint64_t t0 = globaltimer();
     deadline = t0 + a.timeout_ns;
+    s_zc_src = nullptr;
     if (a.rec && blockIdx.x == 0)
       fill_record(a.rec, (long long)t0, a.rec_src, a.rec_dst, -1, 1, a.seq, a.mb, a.bytes);
     if (!wait_geq<kSys>(a.hdr_flag, a.seq, deadline)) {
@@ -344,19 +346,33 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(RecvArgs a) {
       } else if (h->bytes != a.bytes) {
         latch(a.err, PPC_ERR_SIZE_MISMATCH, a.seq, 0x100u);
         fail = 1;
+      } else if (h->flags & kHdrZeroCopy) {
+        const uint32_t seg = h->src_seg;
+        const uint64_t base = (a.seg_tab && seg < (uint32_t)kMaxSeg) ? a.seg_tab[seg] : 0;
+        if (!base) {                   // the receiver never imported that registration
+          latch(a.err, PPC_ERR_ORDER, a.seq, 0x300u | seg << 12);
+          fail = 1;
+        } else {
+          s_zc_src = reinterpret_cast<const uint8_t*>(base + h->src_off);
+        }
       }
     }
   }
   if (__syncthreads_or(fail)) return;
+  const uint8_t* zc_src = s_zc_src;
   for (uint32_t c = blockIdx.x; c < a.n_chunks; c += gridDim.x) {
+    const uint64_t off = (uint64_t)c * a.chunk;
+    const uint64_t len = min(a.chunk, a.bytes - off);
+    if (zc_src) {                      // payload complete at publication: pull it over NVLink
+      cta_copy<true>(a.dst + off, zc_src + off, len);
+      continue;
+    }
     int f = 0;
     if (threadIdx.x == 0 && !wait_geq<kSys>(a.flags + c, a.seq, deadline)) {
       latch(a.err, PPC_ERR_TIMEOUT, a.seq, 0x100u | c << 12);
       f = 1;
     }
     if (__syncthreads_or(f)) return;
-    const uint64_t off = (uint64_t)c * a.chunk;
-    const uint64_t len = min(a.chunk, a.bytes - off);
     cta_copy<true>(a.dst + off, a.src + off, len);
   }
   __threadfence();                 // slot reads + user-buffer writes before the credit
@@ -369,6 +385,38 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(RecvArgs a) {
       if (a.rec) a.rec->t_end_ns = (long long)globaltimer();
     }
   }
+}
+
+// ---------------------------------------------------------------- zero-copy publication
+// The payload stays in the sender's registered buffer; one thread waits for the slot's
+// credit and publishes (segment, offset) in the receiver's slot header.  The stream then
+// waits for the receiver's credit (launch_wait_credit) before the buffer may be reused.
+__global__ void publish_kernel(PublishArgs a) {
+  const uint64_t t0 = globaltimer();
+  if (a.need_credit && !wait_geq(a.credit, a.need_credit, t0 + a.timeout_ns)) {
+    latch(a.err, PPC_ERR_TIMEOUT, a.seq, a.dir);
+    return;
+  }
+  SlotHeader h = {};
+  h.magic = kMagic;
+  h.dir = (uint8_t)a.dir;
+  h.boundary = (uint8_t)a.boundary;
+  h.flags = kHdrZeroCopy;
+  h.bytes = a.bytes;
+  h.seq = a.seq;
+  h.mb = a.mb;
+  h.src_off = a.src_off;
+  h.src_seg = a.src_seg;
+  const uint4* hs = reinterpret_cast<const uint4*>(&h);
+  uint4* hd = reinterpret_cast<uint4*>(a.hdr);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) st_data(hd + j, hs[j]);
+  st_release_sys(a.hdr_flag, a.seq);   // cumulative: the producer's writes to the buffer too
+}
+
+cudaError_t launch_publish(const PublishArgs& a, cudaStream_t s) {
+  publish_kernel<<<1, 1, 0, s>>>(a);
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- K12: CE signalling

@@ -174,6 +174,51 @@ def case_toy(rank, world, bf16=True, steps=5):
     return comm
 
 
+def case_zc(rank, world):
+    """Zero-copy pulls from registered send buffers: ragged sizes byte-exact, then an identity
+    1F1B step whose X / G sources are registered (the receiver pulls them over NVLink)."""
+    cfg = ppc.make_config(pp=world, max_msg_bytes=8 << 20, chunk_bytes=256 << 10)
+    comm = ppc.connect_distributed(cfg, rank, world, rank, with_nccl=False)
+    s = torch.cuda.current_stream()
+    sizes = [1, 4096 + 3, 3 * (256 << 10) + 5, 8 << 20]
+    src = [buf(n) for n in sizes]
+    for i, (b, n) in enumerate(zip(src, sizes)):
+        ppc.fill_payload(b, n, 42, 0, 0, rank, i)
+    ppc.register_tensors(comm, src)
+    for rep in range(3):
+        for i, n in enumerate(sizes):
+            mb = rep * len(sizes) + i
+            for d in (ppc.FWD, ppc.BWD):
+                if (d == ppc.FWD and rank == 0) or (d == ppc.BWD and rank == 1):
+                    comm.send(d, src[i], n, mb=mb, stream=s)
+                elif (d == ppc.FWD and rank == 1) or (d == ppc.BWD and rank == 0):
+                    out = buf(n)
+                    comm.recv(d, out, n, mb=mb, stream=s)
+                    want = P.payload_bytes(42, 0, 0, 1 - rank, i, n)
+                    assert np.array_equal(host(out)[:n], want), (rank, d, n, mb)
+    torch.cuda.synchronize()
+    assert comm.poll() == 0
+    M, n = 4, 2 * (256 << 10) + 77
+    X = [buf(n) for _ in range(M)] if rank == 0 else None
+    G = [buf(n) for _ in range(M)] if rank == 1 else None
+    for m in range(M):
+        if X:
+            ppc.fill_payload(X[m], n, 42, 0, P.SRC_BOUNDARY, 0, m)
+        if G:
+            ppc.fill_payload(G[m], n, 42, 0, P.SRC_BOUNDARY, 1, m)
+    ppc.register_tensors(comm, X or G)
+    out = [buf(n) for _ in range(M)]
+    args = ppc.StepArgs(M, n, n, x=X, g=G, y=out if rank == 1 else None, dx=out if rank == 0 else None)
+    for _ in range(2):
+        ppc.step_1f1b(comm, args, s)
+    torch.cuda.synchronize()
+    assert comm.poll() == 0
+    for m in range(M):
+        ref = P.source_gradient(42, 0, m, n) if rank == 0 else P.source_activation(42, 0, m, n)
+        assert np.array_equal(host(out[m])[:n], ref), (rank, m)
+    return comm
+
+
 def case_hetero(rank, world):
     """NEXT-2: hetero allreduce = NCCL in each stage's DP subgroup + leader exchange over the
     PP path + NCCL broadcast; compared exactly (integer-valued fp32) with the oracle."""
@@ -219,6 +264,8 @@ def main():
         comm = case_toy(rank, world)
     elif case == "hetero":
         comm = case_hetero(rank, world)
+    elif case == "zc":
+        comm = case_zc(rank, world)
     elif case == "dcbs":
         comm = case_dcbs(rank, world)
     else:

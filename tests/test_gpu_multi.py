@@ -43,3 +43,7 @@ def test_dcbs_pp2_tp2():
 @pytest.mark.parametrize("n", [2, 4])
 def test_hetero_allreduce(n):
     _run("hetero", n)
+
+
+def test_zero_copy_registered_pull():
+    _run("zc", 2)

@@ -19,6 +19,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--out", default="gpurun_out/tune.jsonl")
 ap.add_argument("--sm", default="131072,262144,524288,1048576:32,64,128:64,128")
 ap.add_argument("--pull", default="131072,262144,1048576:32,64,128:128")
+ap.add_argument("--zc", default="262144,524288,1048576:32,64,128")
 ap.add_argument("--steps", type=int, default=20)
 a = ap.parse_args()
 rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -33,11 +34,14 @@ s = torch.cuda.current_stream()
 fh = open(a.out, "w") if rank == 0 else None
 
 
-def run(engine, chunk, cta, extra_env):
+def run(engine, chunk, cta, extra_env, zc=False):
     for k, v in extra_env.items():
         os.environ[k] = str(v)
     cfg = ppc.make_config(pp=2, max_msg_bytes=n, chunk_bytes=chunk, engine=engine, cta_per_channel=cta)
     comm = ppc.connect_distributed(cfg, rank, world, rank, with_nccl=False)
+    if zc:
+        ppc.register_tensors(comm, X or G)
+    extra_env = dict(extra_env, zc=int(zc))
     for _ in range(3):
         ppc.step_1f1b(comm, sa, s)
     torch.cuda.synchronize()
@@ -76,4 +80,6 @@ for chunk, cta, rc in grid(a.sm):
     run(ppc.ENGINE_SM, chunk, cta, {"PPC_RECV_CTAS": rc})
 for chunk, cta, st in grid(a.pull):
     run(ppc.ENGINE_PULL, chunk, cta, {"PPC_STAGE_CTAS": st})
+for chunk, rc in grid(a.zc):     # zero-copy pulls: chunk = pull grain, rc = pulling CTAs
+    run(ppc.ENGINE_SM, chunk, 0, {"PPC_RECV_CTAS": rc}, zc=True)
 dist.destroy_process_group()
