@@ -42,7 +42,8 @@ def parse():
     ap.add_argument("--hidden", type=int, default=4096)
     ap.add_argument("--engine", default="sm", choices=["sm", "ce", "pull"])
     ap.add_argument("--chunk", type=int, default=0,
-                    help="flag granularity; 0 = 512 KiB across NVLink, 128 KiB for virtual stages")
+                    help="flag / pull granularity; 0 = tuned default (256 KiB zero-copy, "
+                         "512 KiB ring push, 128 KiB virtual stages)")
     ap.add_argument("--channels", type=int, default=1)
     ap.add_argument("--cta", type=int, default=0)
     ap.add_argument("--slots", type=int, default=2)
@@ -206,7 +207,8 @@ def main():
     dev = torch.cuda.current_device()
     if not args.chunk:
         # tuned on 2x B200 (profiles/r1_tune_step_ws.jsonl): 512 KiB chunks x 64 CTAs
-        args.chunk = (512 << 10) if distributed else (128 << 10)
+        # zero-copy pulls: 256 KiB grain; ring push: 512 KiB (profiles/r11_tune.jsonl)
+        args.chunk = ((256 if args.zc else 512) << 10) if distributed else (128 << 10)
     S = args.pp
     nbytes = args.seq * args.hidden * 2
     M = args.M
@@ -322,8 +324,13 @@ def main():
         unit, bound = "GB/s", "hbm"
         peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
     achieved = alg / (avg_push_ms * 1e-3) / 1e9
-    kname = "ppc::push_ws_kernel (SM push over NVLink)" if distributed else \
-        "ppc::copy_kernel (virtual-stage single-copy hand-off)"
+    if not distributed:
+        kname = "ppc::copy_kernel (virtual-stage single-copy hand-off)"
+    elif args.zc:
+        kname = ("zero-copy send op: publish_kernel -> receiver recv_kernel NVLink pull -> "
+                 "credit (CUDA events on the sender stream bracket the whole transfer)")
+    else:
+        kname = "ppc::push_ws_kernel (SM push over NVLink)"
     roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
             "frac": achieved / peak, "traffic": ncu_traffic("push_n%d" % min(world, 2)),
             "kernel": kname, "alg_bytes_per_launch": alg,
