@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--channels", type=int, default=1)
     ap.add_argument("--cta", type=int, default=0)
     ap.add_argument("--slots", type=int, default=2)
+    ap.add_argument("--graph", type=int, default=1,
+                    help="replay the step as one CUDA graph (ppc_graph_create)")
     ap.add_argument("--zc", type=int, default=1,
                     help="N>=2: register the step's send buffers (zero-copy NVLink pulls)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -183,6 +185,7 @@ def workload_config(args, pipelines, virtual):
             "seq": args.seq, "hidden": args.hidden, "msg_bytes": args.seq * args.hidden * 2,
             "engine": args.engine, "chunk_bytes": args.chunk, "channels": args.channels,
             "ring_slots": args.slots, "zero_copy_sends": bool(args.zc) and not virtual,
+            "cuda_graph": bool(args.graph),
             "l2": "inputs larger than L2 (M x 32 MiB per stage per direction, 256 MiB)"}
 
 
@@ -248,7 +251,12 @@ def main():
         # zero-copy: the stage inputs X / G are registered send buffers; receivers pull them
         ppc.register_tensors(comms[0], [t for s in stages for t in X.get(s, []) + G.get(s, [])])
 
-    def one_step(a=None):
+    graph = [None]
+
+    def one_step(a=None, eager=False):
+        if graph[0] is not None and a is None and not eager:
+            graph[0].launch()
+            return
         a = a or args_dev
         if distributed:
             ppc.step_1f1b(comms[0], a[0], streams[0])
@@ -267,24 +275,30 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    one_step(eager=True)                 # allocates the step buffers
+    barrier()
+    if args.graph:                       # the whole step as one CUDA graph per process
+        graph[0] = ppc.StepGraph(comms, args_dev, streams)
     for _ in range(args.warmup):
         one_step()
     barrier()
 
     def timed_region(instrumented: bool):
-        """K steps between barriers + synchronize; CUDA events on every stage stream;
-        max over ranks.  instrumented: CUDA-event pairs around every transfer launch."""
+        """K steps between barriers + synchronize; CUDA events on every stage stream (the
+        launch stream for graph replays); max over ranks.  instrumented: eager steps with
+        CUDA-event pairs around every transfer launch."""
         for c in comms:
             c.set_trace(2 if instrumented else 0)
             c.kernel_times(0), c.kernel_times(1)
-        ev0 = [torch.cuda.Event(enable_timing=True) for _ in stages]
-        ev1 = [torch.cuda.Event(enable_timing=True) for _ in stages]
+        sts = streams[:1] if (graph[0] is not None and not instrumented) else streams
+        ev0 = [torch.cuda.Event(enable_timing=True) for _ in sts]
+        ev1 = [torch.cuda.Event(enable_timing=True) for _ in sts]
         barrier()
-        for e, st in zip(ev0, streams):
+        for e, st in zip(ev0, sts):
             e.record(st)
         for _ in range(args.steps):
-            one_step()
-        for e, st in zip(ev1, streams):
+            one_step(eager=instrumented)
+        for e, st in zip(ev1, sts):
             e.record(st)
         barrier()
         return max_over_ranks(max(a.elapsed_time(b) for a, b in zip(ev0, ev1)))
@@ -409,6 +423,8 @@ def main():
         }
         print(json.dumps(line), flush=True)
     barrier()
+    if graph[0] is not None:
+        graph[0].destroy()
     for c in comms:
         c.disconnect()
     if distributed:

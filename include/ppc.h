@@ -192,6 +192,20 @@ ppc_status_t ppc_step_1f1b(ppc_comm_t* c, const ppc_step_t* st, cudaStream_t s);
 ppc_status_t ppc_step_1f1b_local(ppc_comm_t* const* comms, int S, const ppc_step_t* steps,
                                  const cudaStream_t* streams);
 
+/* CUDA-graph capture of one 1F1B step (streams and graphs instead of per-op launches).
+ * n == 1: comms[0] is a one-process-per-GPU comm, the step is ppc_step_1f1b(comms[0],
+ * &steps[0], streams[0]); n == S: virtual stages, ppc_step_1f1b_local(comms, S, steps,
+ * streams).  Every kernel of the captured step reads its sequence number relative to a
+ * device counter that ppc_graph_launch sets, so one graph replays every later step; the
+ * host counters advance per launch exactly as an eager step would.  The step arguments'
+ * buffers must stay valid for the graph's lifetime.  Not capturable: the CE engine.  Before
+ * creating, the devices are synchronised; launches are serialised on streams[0]. */
+typedef struct ppc_graph ppc_graph_t;
+ppc_status_t ppc_graph_create(ppc_comm_t* const* comms, int n, const ppc_step_t* steps,
+                              const cudaStream_t* streams, ppc_graph_t** out);
+ppc_status_t ppc_graph_launch(ppc_graph_t* g);
+ppc_status_t ppc_graph_destroy(ppc_graph_t* g);
+
 /* DCBS TP/DP traffic on NCCL: in-place sum allreduce over group g.
  * PPC_ERR_BACKEND for g == PPC_GROUP_PP. nccl_dtype is an ncclDataType_t value. */
 ppc_status_t ppc_allreduce(ppc_comm_t* c, ppc_group_t g, void* buf, size_t count,

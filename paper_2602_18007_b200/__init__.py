@@ -97,6 +97,10 @@ _step = _sig("ppc_step_1f1b", _i, [_vp, C.POINTER(Step), _vp])
 _step_local = _sig("ppc_step_1f1b_local", _i, [C.POINTER(_vp), _i, C.POINTER(Step), C.POINTER(_vp)])
 _allreduce = _sig("ppc_allreduce", _i, [_vp, _i, _vp, _sz, _i, _vp])
 _hx_allreduce = _sig("ppc_hetero_allreduce", _i, [_vp, _vp, _sz, _i, _vp])
+_graph_create = _sig("ppc_graph_create", _i, [C.POINTER(_vp), _i, C.POINTER(Step), C.POINTER(_vp),
+                                              C.POINTER(_vp)])
+_graph_launch = _sig("ppc_graph_launch", _i, [_vp])
+_graph_destroy = _sig("ppc_graph_destroy", _i, [_vp])
 _register = _sig("ppc_register", _i, [_vp, _vp, _sz, _vp, C.POINTER(_sz)])
 _reg_import = _sig("ppc_register_import", _i, [_vp, _vp, _sz])
 REG_BLOB_BYTES = 128
@@ -320,6 +324,30 @@ def step_1f1b_local(comms, args, streams):
     steps = (Step * S)(*[a.st for a in args])
     ss = (C.c_void_p * S)(*[_stream(s) for s in streams])
     _check(_step_local(hs, S, steps, ss), "ppc_step_1f1b_local")
+
+
+class StepGraph:
+    """One 1F1B step captured into a CUDA graph (ppc_graph_create); launch() replays the next
+    step.  comms/args/streams as for step_1f1b (one comm) or step_1f1b_local (S comms).
+    Run one eager step before creating it (the step's buffers must exist)."""
+
+    def __init__(self, comms, args, streams):
+        comms, args, streams = list(comms), list(args), list(streams)
+        self._keep = (comms, args)
+        self._steps = (Step * len(args))(*[a.st for a in args])
+        hs = (C.c_void_p * len(comms))(*[c.h.value for c in comms])
+        ss = (C.c_void_p * len(streams))(*[_stream(s) for s in streams])
+        h = C.c_void_p()
+        _check(_graph_create(hs, len(comms), self._steps, ss, C.byref(h)), "ppc_graph_create")
+        self.h = h
+
+    def launch(self):
+        _check(_graph_launch(self.h), "ppc_graph_launch")
+
+    def destroy(self):
+        if self.h:
+            _check(_graph_destroy(self.h), "ppc_graph_destroy")
+            self.h = None
 
 
 def fill_payload(buf, nbytes=None, seed=42, step=0, boundary=0, direction=0, mb=0, stream=None):

@@ -368,7 +368,10 @@ ppc_status_t ppc_pp_send(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_t byt
     if (need) {
       Chan& rh = h.out_comm->ch[d];
       if (rh.recv_seq < need) return PPC_ERR_WOULD_BLOCK;
-      CK(cudaStreamWaitEvent(s, rh.recvd_ev[slot], 0));
+      // while capturing a graph, a recv enqueued before the capture belongs to an earlier
+      // (already serialised) launch: no edge
+      if (!(c->capturing && need <= h.out_comm->cap_recv[d]))
+        CK(cudaStreamWaitEvent(s, rh.recvd_ev[slot], 0));
     }
     need = 0;   // ordered by the event; the kernel does not spin on the same GPU
   }
@@ -395,8 +398,17 @@ ppc_status_t ppc_pp_send(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_t byt
     p.boundary = (uint32_t)boundary;
     p.err = c->err_dev;
     p.timeout_ns = c->timeout_ns;
+    const uint64_t* base = nullptr;
+    uint64_t target = seq;
+    if (c->capturing) {           // graph: relative seq, slot resolved on device
+      base = c->dseq + d;
+      p.sr = {base, 0, (uint32_t)c->K, 0, c->local_mode ? 0u : 1u, 0};
+      p.seq = target = seq - c->cap_send[d];
+      p.hdr = h.o_hdr;
+      p.hdr_flag = h.o_hdr_flag;
+    }
     CK(launch_publish(p, s));
-    CK(launch_wait_credit(h.credit, seq, c->err_dev, c->timeout_ns, s));   // rendezvous
+    CK(launch_wait_credit(h.credit, target, c->err_dev, c->timeout_ns, s, base));   // rendezvous
   } else if (c->cfg.engine != PPC_ENGINE_CE || bytes == 0) {  // SM push, or PULL's staging
     PushArgs a{};
     a.src = static_cast<const uint8_t*>(buf);
@@ -420,8 +432,18 @@ ppc_status_t ppc_pp_send(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_t byt
     a.rec_src = c->rank;
     a.rec_dst = h.peer_out;
     a.done = h.push_done;
+    if (c->capturing) {           // graph: relative seq, slot resolved on device
+      a.sr = {c->dseq + d, (uint64_t)c->lay.stride, (uint32_t)c->K,
+              std::max<uint32_t>(c->lay.max_chunks, 1), c->local_mode ? 0u : 1u, 0};
+      a.seq = seq - c->cap_send[d];
+      a.dst = h.o_payload;
+      a.hdr = h.o_hdr;
+      a.hdr_flag = h.o_hdr_flag;
+      a.flags = h.o_flags;
+    }
     CK(launch_push(a, push_grid(c, n_chunks), c->sys_scope, env_int("PPC_PUSH_WS", 1) != 0, s));
   } else {
+    if (c->capturing) return PPC_ERR_INVALID_ARG;       // CE copies are not graph-relocatable
     CeHeadArgs a{};
     a.hdr = h.o_hdr + slot;
     a.hdr_flag = h.o_hdr_flag + slot;
@@ -476,7 +498,8 @@ ppc_status_t ppc_pp_recv(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t bytes, lo
   if (c->local_mode) {
     Chan& sh = h.in_comm->ch[d];
     if (sh.send_seq < seq) return PPC_ERR_WOULD_BLOCK;
-    CK(cudaStreamWaitEvent(s, sh.sent_ev[slot], 0));
+    if (!(c->capturing && seq <= h.in_comm->cap_send[d]))
+      CK(cudaStreamWaitEvent(s, sh.sent_ev[slot], 0));
   }
   const uint32_t n_chunks = (uint32_t)((bytes + c->chunk - 1) / c->chunk);
   RecvArgs a{};
@@ -498,6 +521,16 @@ ppc_status_t ppc_pp_recv(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t bytes, lo
   a.rec_src = h.peer_in;
   a.rec_dst = c->rank;
   a.seg_tab = c->seg_tab ? c->seg_tab + (d == PPC_FWD ? 0 : 1) * kMaxSeg : nullptr;
+  if (c->capturing) {             // graph: relative seq, slot resolved on device
+    a.sr = {c->dseq + 2 + d, (uint64_t)c->lay.stride, (uint32_t)c->K,
+            std::max<uint32_t>(c->lay.max_chunks, 1), 0, 0};
+    a.seq = seq - c->cap_recv[d];
+    a.src = h.i_payload;
+    a.hdr = h.i_hdr;
+    a.hdr_flag = h.i_hdr_flag;
+    a.flags = h.i_flags;
+    a.done = h.i_done;
+  }
   if (ppc_status_t ts = time_mark(c, 1, s, true)) return ts;
   CK(launch_recv(a, recv_grid(c, n_chunks), c->sys_scope, s));
   if (ppc_status_t ts = time_mark(c, 1, s, false)) return ts;
@@ -518,10 +551,15 @@ ppc_status_t ppc_pp_wait_consumed(ppc_comm_t* c, ppc_dir_t d, cudaStream_t s) {
   if (c->local_mode) {
     Chan& rh = h.out_comm->ch[d];
     if (rh.recv_seq < h.send_seq) return PPC_ERR_WOULD_BLOCK;
-    CK(cudaStreamWaitEvent(s, rh.recvd_ev[h.send_seq % c->K], 0));
+    if (!(c->capturing && h.send_seq <= h.out_comm->cap_recv[d]))
+      CK(cudaStreamWaitEvent(s, rh.recvd_ev[h.send_seq % c->K], 0));
     return PPC_OK;
   }
-  CK(launch_wait_credit(h.credit, h.send_seq, c->err_dev, c->timeout_ns, s));
+  if (c->capturing)
+    CK(launch_wait_credit(h.credit, h.send_seq - c->cap_send[d], c->err_dev, c->timeout_ns, s,
+                          c->dseq + d));
+  else
+    CK(launch_wait_credit(h.credit, h.send_seq, c->err_dev, c->timeout_ns, s));
   return PPC_OK;
 }
 
@@ -739,6 +777,7 @@ ppc_status_t ppc_destroy(ppc_comm_t* c) {
       for (cudaEvent_t e : c->tev[k]) cudaEventDestroy(e);
     if (c->hx_buf) cudaFree(c->hx_buf);
     if (c->seg_tab) cudaFree(c->seg_tab);
+    if (c->dseq) cudaFree(c->dseq);
     if (c->arena) cudaFree(c->arena);
     if (c->err_host) cudaFreeHost(c->err_host);
   }

@@ -140,6 +140,12 @@ struct ppc_comm {
   std::vector<Reg> regs;
   uint64_t* seg_tab = nullptr;    // device [2][kMaxSeg]: 0 = from prev (FWD in), 1 = next
   std::vector<void*> reg_opened;
+  // CUDA-graph capture (ppc_graph_create): sends / receives enqueued while capturing use
+  // sequence numbers relative to cap_*; dseq = {send FWD, send BWD, recv FWD, recv BWD}
+  // device bases, set before each graph launch
+  bool capturing = false;
+  uint64_t cap_send[2] = {0, 0}, cap_recv[2] = {0, 0};
+  uint64_t* dseq = nullptr;
   Blob blob{};
 };
 

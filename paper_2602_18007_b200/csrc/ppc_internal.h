@@ -34,7 +34,20 @@ struct ErrWord {
   unsigned int code, seq, info, pad;
 };
 
+// Graph-capturable sequence numbers.  base == nullptr: `seq` in the kernel args is absolute
+// and every slot pointer is already resolved by the host.  Otherwise (a captured CUDA graph)
+// seq = args.seq + *base, where *base is a device counter set before each graph launch, and
+// the kernel resolves the slot (seq % K) pointers from the slot-0 bases itself.
+struct SeqRef {
+  const uint64_t* base;
+  uint64_t stride;             // payload bytes per slot
+  uint32_t K, fstride;         // slots; chunk flags per slot
+  uint32_t wait_credit;        // wait credit >= seq - K (cross-GPU) or not (virtual stages)
+  uint32_t pad;
+};
+
 struct PushArgs {
+  SeqRef sr;
   const uint8_t* src;
   uint8_t* dst;                 // peer (or local) slot payload
   SlotHeader* hdr;              // peer slot header
@@ -56,6 +69,7 @@ struct PushArgs {
 };
 
 struct RecvArgs {
+  SeqRef sr;
   uint8_t* dst;                 // user buffer
   const uint8_t* src;           // local slot payload
   const SlotHeader* hdr;
@@ -76,6 +90,7 @@ struct RecvArgs {
 
 // Zero-copy publication of a registered send buffer: credit wait, header, header flag.
 struct PublishArgs {
+  SeqRef sr;
   SlotHeader* hdr;
   uint64_t* hdr_flag;
   const uint64_t* credit;
@@ -123,8 +138,13 @@ cudaError_t launch_add(void* dst, const void* src, size_t count, int dtype, cuda
 // Same-GPU single copy (direct mode of virtual stages): dst <- src, `bytes`, CTA chunks.
 cudaError_t launch_copy(void* dst, const void* src, uint64_t bytes, uint64_t chunk, int grid,
                         cudaStream_t s);
+// wait until *credit >= target (+ *seq_base when seq_base != nullptr: graph replay)
 cudaError_t launch_wait_credit(const uint64_t* credit, uint64_t target, ErrWord* err,
-                               uint64_t timeout_ns, cudaStream_t s);
+                               uint64_t timeout_ns, cudaStream_t s,
+                               const uint64_t* seq_base = nullptr);
+// graph launch prologue: seq[0..3] = v[0..3]
+cudaError_t launch_set_seq(uint64_t* seq, uint64_t v0, uint64_t v1, uint64_t v2, uint64_t v3,
+                           cudaStream_t s);
 cudaError_t launch_recv(const RecvArgs& a, int grid, bool sys, cudaStream_t s);
 cudaError_t launch_ce_head(const CeHeadArgs& a, cudaStream_t s);
 cudaError_t launch_ce_flags(uint64_t* flags, uint32_t c0, uint32_t c1, uint64_t seq,

@@ -170,9 +170,47 @@ __device__ __forceinline__ void cta_copy(uint8_t* __restrict__ dst, const uint8_
   }
 }
 
+// ---------------------------------------------------------------- graph-replay resolution
+// (SeqRef): absolute seq and slot pointers from the device sequence base.
+__device__ __forceinline__ PushArgs resolve(PushArgs a) {
+  if (a.sr.base) {
+    a.seq += *a.sr.base;
+    const uint64_t slot = a.seq % a.sr.K;
+    a.dst += slot * a.sr.stride;
+    a.hdr += slot;
+    a.hdr_flag += slot;
+    a.flags += slot * a.sr.fstride;
+    a.need_credit = (a.sr.wait_credit && a.seq > a.sr.K) ? a.seq - a.sr.K : 0;
+  }
+  return a;
+}
+__device__ __forceinline__ RecvArgs resolve(RecvArgs a) {
+  if (a.sr.base) {
+    a.seq += *a.sr.base;
+    const uint64_t slot = a.seq % a.sr.K;
+    a.src += slot * a.sr.stride;
+    a.hdr += slot;
+    a.hdr_flag += slot;
+    a.flags += slot * a.sr.fstride;
+    a.done += slot;
+  }
+  return a;
+}
+__device__ __forceinline__ PublishArgs resolve(PublishArgs a) {
+  if (a.sr.base) {
+    a.seq += *a.sr.base;
+    const uint64_t slot = a.seq % a.sr.K;
+    a.hdr += slot;
+    a.hdr_flag += slot;
+    a.need_credit = (a.sr.wait_credit && a.seq > a.sr.K) ? a.seq - a.sr.K : 0;
+  }
+  return a;
+}
+
 // ---------------------------------------------------------------- K9: push (SM engine)
 template <bool kSys>
-__global__ void __launch_bounds__(kThreads) push_kernel(PushArgs a) {
+__global__ void __launch_bounds__(kThreads) push_kernel(PushArgs a0) {
+  const PushArgs a = resolve(a0);
   uint64_t deadline = 0;
   int fail = 0;
   if (threadIdx.x == 0) {
@@ -253,7 +291,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
 }
 
 template <bool kSys>
-__global__ void __launch_bounds__(kWsThreads) push_ws_kernel(PushArgs a) {
+__global__ void __launch_bounds__(kWsThreads) push_ws_kernel(PushArgs a0) {
+  const PushArgs a = resolve(a0);
   __shared__ __align__(8) uint64_t full[kWsRing], empty[kWsRing];
   uint64_t deadline = 0;
   int fail = 0;
@@ -325,7 +364,8 @@ __global__ void __launch_bounds__(kWsThreads) push_ws_kernel(PushArgs a) {
 
 // ---------------------------------------------------------------- K10: recv + copy-out
 template <bool kSys>
-__global__ void __launch_bounds__(kThreads) recv_kernel(RecvArgs a) {
+__global__ void __launch_bounds__(kThreads) recv_kernel(RecvArgs a0) {
+  const RecvArgs a = resolve(a0);
   __shared__ const uint8_t* s_zc_src;   // zero-copy: the sender's buffer, mapped here
   uint64_t deadline = 0;
   int fail = 0;
@@ -391,7 +431,8 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(RecvArgs a) {
 // The payload stays in the sender's registered buffer; one thread waits for the slot's
 // credit and publishes (segment, offset) in the receiver's slot header.  The stream then
 // waits for the receiver's credit (launch_wait_credit) before the buffer may be reused.
-__global__ void publish_kernel(PublishArgs a) {
+__global__ void publish_kernel(PublishArgs a0) {
+  const PublishArgs a = resolve(a0);
   const uint64_t t0 = globaltimer();
   if (a.need_credit && !wait_geq(a.credit, a.need_credit, t0 + a.timeout_ns)) {
     latch(a.err, PPC_ERR_TIMEOUT, a.seq, a.dir);
@@ -452,8 +493,22 @@ __global__ void ce_flags_kernel(uint64_t* flags, uint32_t c0, uint32_t c1, uint6
 
 // Wait until the receiver consumed `target` (credit protocol), bounded.
 __global__ void wait_credit_kernel(const uint64_t* credit, uint64_t target, ErrWord* err,
-                                   uint64_t timeout_ns) {
+                                   uint64_t timeout_ns, const uint64_t* seq_base) {
+  if (seq_base) target += *seq_base;
   if (!wait_geq(credit, target, globaltimer() + timeout_ns)) latch(err, PPC_ERR_TIMEOUT, target, 0x200u);
+}
+
+__global__ void set_seq_kernel(uint64_t* seq, uint64_t v0, uint64_t v1, uint64_t v2, uint64_t v3) {
+  seq[0] = v0;
+  seq[1] = v1;
+  seq[2] = v2;
+  seq[3] = v3;
+}
+
+cudaError_t launch_set_seq(uint64_t* seq, uint64_t v0, uint64_t v1, uint64_t v2, uint64_t v3,
+                           cudaStream_t s) {
+  set_seq_kernel<<<1, 1, 0, s>>>(seq, v0, v1, v2, v3);
+  return cudaGetLastError();
 }
 
 template <typename T>
@@ -497,8 +552,8 @@ cudaError_t launch_copy(void* dst, const void* src, uint64_t bytes, uint64_t chu
 }
 
 cudaError_t launch_wait_credit(const uint64_t* credit, uint64_t target, ErrWord* err,
-                               uint64_t timeout_ns, cudaStream_t s) {
-  wait_credit_kernel<<<1, 1, 0, s>>>(credit, target, err, timeout_ns);
+                               uint64_t timeout_ns, cudaStream_t s, const uint64_t* seq_base) {
+  wait_credit_kernel<<<1, 1, 0, s>>>(credit, target, err, timeout_ns, seq_base);
   return cudaGetLastError();
 }
 

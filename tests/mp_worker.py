@@ -219,6 +219,70 @@ def case_zc(rank, world):
     return comm
 
 
+def case_graph(rank, world, zc=False):
+    """A 1F1B step captured into a CUDA graph across processes (device-side sequence bases):
+    XOR step graph launches interleaved with eager steps; then an identity step whose X / G
+    are registered (zero-copy pulls inside the graph)."""
+    S, M, n = world, 4, 3 * (256 << 10) + 99
+    cfg = ppc.make_config(pp=S, max_msg_bytes=n, chunk_bytes=256 << 10)
+    comm = ppc.connect_distributed(cfg, rank, world, rank, with_nccl=False)
+    s = torch.cuda.current_stream()
+    X = [buf(n) for _ in range(M)] if rank == 0 else None
+    G = [buf(n) for _ in range(M)] if rank == S - 1 else None
+    out = [buf(n) for _ in range(M)]
+    for m in range(M):
+        if X:
+            ppc.fill_payload(X[m], n, 42, 0, P.SRC_BOUNDARY, 0, m)
+        if G:
+            ppc.fill_payload(G[m], n, 42, 0, P.SRC_BOUNDARY, 1, m)
+    fctx, bctx = ppc.XorCtx(42, 0, rank, 0), ppc.XorCtx(42, 0, rank, 1)
+    xargs = ppc.StepArgs(M, n, n, fwd=ppc.STAGE_XOR, bwd=ppc.STAGE_XOR, fwd_user=fctx,
+                         bwd_user=bctx, x=X, g=G, y=out if rank == S - 1 else None,
+                         dx=out if rank == 0 else None)
+    mask = lambda st, d, m: P.proxy_mask(42, 0, st, d, m, n)
+
+    def check_xor():
+        torch.cuda.synchronize()
+        assert comm.poll() == 0, ppc.STATUS[comm.poll()]
+        if rank in (0, S - 1):
+            for m in range(M):
+                y, g = xor_closed_form(S, m, P.source_activation(42, 0, m, n),
+                                       P.source_gradient(42, 0, m, n), mask)
+                assert np.array_equal(host(out[m])[:n], y if rank == S - 1 else g), (rank, m)
+                out[m].fill_(0)
+
+    ppc.step_1f1b(comm, xargs, s)
+    check_xor()
+    dist.barrier()
+    graph = ppc.StepGraph([comm], [xargs], [s])
+    for it in range(4):
+        graph.launch()
+        check_xor()
+        if it == 1:
+            ppc.step_1f1b(comm, xargs, s)      # eager step between graph launches
+            check_xor()
+    graph.destroy()
+    # identity step with registered sources: zero-copy pulls captured in the graph
+    ppc.register_tensors(comm, X or G)
+    iargs = ppc.StepArgs(M, n, n, x=X, g=G, y=out if rank == S - 1 else None,
+                         dx=out if rank == 0 else None)
+    ppc.step_1f1b(comm, iargs, s)
+    torch.cuda.synchronize()
+    dist.barrier()
+    g2 = ppc.StepGraph([comm], [iargs], [s])
+    for _ in range(3):
+        g2.launch()
+        torch.cuda.synchronize()
+        assert comm.poll() == 0
+        if rank in (0, S - 1):
+            for m in range(M):
+                ref = P.source_gradient(42, 0, m, n) if rank == 0 else P.source_activation(42, 0, m, n)
+                assert np.array_equal(host(out[m])[:n], ref), (rank, m)
+                out[m].fill_(0)
+    g2.destroy()
+    return comm
+
+
 def case_hetero(rank, world):
     """NEXT-2: hetero allreduce = NCCL in each stage's DP subgroup + leader exchange over the
     PP path + NCCL broadcast; compared exactly (integer-valued fp32) with the oracle."""
@@ -266,6 +330,8 @@ def main():
         comm = case_hetero(rank, world)
     elif case == "zc":
         comm = case_zc(rank, world)
+    elif case == "graph":
+        comm = case_graph(rank, world)
     elif case == "dcbs":
         comm = case_dcbs(rank, world)
     else:

@@ -158,6 +158,58 @@ def test_xor_1f1b_step_matches_oracle(S, M, engine, direct, monkeypatch):
 
 
 @pytest.mark.parametrize("direct", [1, 0])
+@pytest.mark.parametrize("S", [2, 3])
+def test_xor_step_cuda_graph(S, direct, monkeypatch):
+    """A step captured into a CUDA graph (relative sequence numbers on device) replays
+    correctly several times, interleaved with eager steps (host counters stay in sync)."""
+    monkeypatch.setenv("PPC_LOCAL_DIRECT", str(direct))
+    M, n = 4, 2 * (64 << 10) + 321
+    cfg = ppc.make_config(pp=S, max_msg_bytes=n, chunk_bytes=64 << 10)
+    comms = ppc.virtual_stages(cfg, DEV)
+    X = [_buf(n) for _ in range(M)]
+    G = [_buf(n) for _ in range(M)]
+    Y = [_buf(n) for _ in range(M)]
+    DX = [_buf(n) for _ in range(M)]
+    for m in range(M):
+        ppc.fill_payload(X[m], n, 42, 0, P.SRC_BOUNDARY, 0, m)
+        ppc.fill_payload(G[m], n, 42, 0, P.SRC_BOUNDARY, 1, m)
+    ctx = [(ppc.XorCtx(42, 0, s, 0), ppc.XorCtx(42, 0, s, 1)) for s in range(S)]
+    args = [ppc.StepArgs(M, n, n, fwd=ppc.STAGE_XOR, bwd=ppc.STAGE_XOR, fwd_user=ctx[s][0],
+                         bwd_user=ctx[s][1], x=X if s == 0 else None, g=G if s == S - 1 else None,
+                         y=Y if s == S - 1 else None, dx=DX if s == 0 else None) for s in range(S)]
+    streams = [torch.cuda.Stream() for _ in range(S)]
+    mask = _masks(n)
+    ref = [xor_closed_form(S, m, P.source_activation(42, 0, m, n), P.source_gradient(42, 0, m, n),
+                           mask) for m in range(M)]
+
+    def check():
+        torch.cuda.synchronize()
+        for m in range(M):
+            assert np.array_equal(_host(Y[m])[:n], ref[m][0]), m
+            assert np.array_equal(_host(DX[m])[:n], ref[m][1]), m
+            Y[m].fill_(0)
+            DX[m].fill_(0)
+
+    ppc.step_1f1b_local(comms, args, streams)        # eager step: allocates step buffers
+    check()
+    g = ppc.StepGraph(comms, args, streams)
+    for _ in range(3):
+        g.launch()
+        check()
+    ppc.step_1f1b_local(comms, args, streams)        # eager again after graph launches
+    check()
+    g.launch()
+    check()
+    for c in comms:
+        assert c.poll() == 0
+    g.destroy()
+    for c in comms:
+        c.disconnect()
+    for c in comms:
+        c.destroy()
+
+
+@pytest.mark.parametrize("direct", [1, 0])
 def test_c2_full_size_sampled(direct, monkeypatch):
     """BASELINE configs[1] shape: [1,4096,4096] bf16 boundary (32 MiB), PP=2, M=8, in the
     launch configuration bench.py times at N=1 (128 KiB chunks, direct single-copy hand-off;

@@ -47,3 +47,8 @@ def test_hetero_allreduce(n):
 
 def test_zero_copy_registered_pull():
     _run("zc", 2)
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_step_cuda_graph(n):
+    _run("graph", n)
