@@ -35,6 +35,7 @@ def parse():
     ap.add_argument("--sm", default="16:1M,32:1M,64:1M,32:256K,64:256K,128:256K,32:4M")
     ap.add_argument("--ce", default="1,2,4,8")
     ap.add_argument("--pull", default="", help="PULL engine specs cta:chunk, e.g. 32:1M,64:1M")
+    ap.add_argument("--zc", default="", help="zero-copy specs recv_ctas:chunk, e.g. 64:256K")
     ap.add_argument("--modes", default="uni,bidir")
     ap.add_argument("--comparators", default="nccl,ce_copy,gloo")
     ap.add_argument("--reps", type=int, default=5)
@@ -55,13 +56,15 @@ def emit(fh, rec):
     fh.flush()
 
 
-def bench_ppc(comm, rank, sizes, modes, label, reps, fh):
+def bench_ppc(comm, rank, sizes, modes, label, reps, fh, zc=False):
     s_send = torch.cuda.Stream()
     s_recv = torch.cuda.Stream()
     maxn = max(sizes)
     src = torch.empty(maxn, dtype=torch.uint8, device="cuda")
     dst = torch.empty(maxn, dtype=torch.uint8, device="cuda")
     ppc.fill_payload(src, maxn, 42, 0, 0, rank, 0)
+    if zc:                       # registered source: receivers pull it over NVLink
+        ppc.register_tensors(comm, [src])
     for mode in modes:
         for n in sizes:
             N = nmsgs(n)
@@ -200,6 +203,19 @@ def main():
         comm = ppc.connect_distributed(cfg, rank, world, torch.cuda.current_device(),
                                        with_nccl=False)
         bench_ppc(comm, rank, sizes, modes, f"ppc_ce_ch{ch}", a.reps, fh)
+        dist.barrier()
+        comm.disconnect()
+        dist.barrier()
+        comm.destroy()
+    for spec in [x for x in a.zc.split(",") if x]:
+        rc, chunk = spec.split(":")
+        os.environ["PPC_RECV_CTAS"] = rc
+        cfg = ppc.make_config(pp=world, max_msg_bytes=maxn, chunk_bytes=size_of(chunk))
+        comm = ppc.connect_distributed(cfg, rank, world, torch.cuda.current_device(),
+                                       with_nccl=False)
+        bench_ppc(comm, rank, sizes, modes, f"ppc_zerocopy_recv{rc}_chunk{chunk}", a.reps, fh,
+                  zc=True)
+        os.environ.pop("PPC_RECV_CTAS")
         dist.barrier()
         comm.disconnect()
         dist.barrier()

@@ -276,6 +276,9 @@ struct Stepper {
   ppc_status_t finish() {
     if (dmode) return PPC_OK;
     for (int d = 0; d < 2; ++d) {
+      // join only the send streams this stage used (an unused one is not part of a graph
+      // capture, and waiting on it from the capturing stream would be illegal)
+      if (!(d == 0 ? s < S - 1 : s > 0)) continue;
       CK(cudaEventRecord(c->sb.join[d], c->side[d]));
       CK(cudaStreamWaitEvent(cs, c->sb.join[d], 0));
     }
