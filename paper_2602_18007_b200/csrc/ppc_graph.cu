@@ -110,11 +110,19 @@ ppc_status_t ppc_graph_create(ppc_comm_t* const* comms, int n, const ppc_step_t*
   }
   cudaGraph_t graph = nullptr;
   const cudaError_t ec = cudaStreamEndCapture(s0, &graph);
+  if (getenv("PPC_DEBUG") && (st || ec != cudaSuccess))
+    fprintf(stderr, "ppc: graph capture step=%d end=%s\n", (int)st, cudaGetErrorString(ec));
   if (!st && ec != cudaSuccess) st = PPC_ERR_CUDA;
   if (fork) cudaEventDestroy(fork);
   for (cudaEvent_t e : joins) if (e) cudaEventDestroy(e);
   finish(st);
-  if (!st && cudaGraphInstantiate(&g->exec, graph, 0) != cudaSuccess) st = PPC_ERR_CUDA;
+  if (!st) {
+    const cudaError_t ei = cudaGraphInstantiate(&g->exec, graph, 0);
+    if (ei != cudaSuccess) {
+      if (getenv("PPC_DEBUG")) fprintf(stderr, "ppc: graph instantiate %s\n", cudaGetErrorString(ei));
+      st = PPC_ERR_CUDA;
+    }
+  }
   g->graph = graph;
   if (st) {
     cudaGetLastError();
