@@ -11,11 +11,37 @@ struct ppc_graph {
   std::vector<cudaStream_t> streams;
   std::vector<uint64_t> dsend[2], drecv[2];       // per comm, messages per step
   std::vector<cudaEvent_t> ev;                    // prologue joins
+  std::vector<cudaEvent_t> captured;              // events referenced by the graph's nodes
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
 };
 
 namespace {
+
+// Events recorded inside a capture become graph nodes and can no longer be waited on by
+// eager work; the graph keeps them (they must outlive it) and the comm gets fresh ones.
+cudaError_t swap_events(ppc_comm* c, std::vector<cudaEvent_t>& keep) {
+  auto swap = [&](cudaEvent_t& e) -> cudaError_t {
+    if (!e) return cudaSuccess;
+    keep.push_back(e);
+    return cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  };
+  StepBufs& sb = c->sb;
+  cudaError_t r = swap(sb.ready);
+  for (int d = 0; d < 2; ++d) {
+    if (!r) r = swap(sb.join[d]);
+    for (int i = 0; i < 2 && !r; ++i) {
+      r = swap(sb.rfree[d][i]);
+      if (!r) r = swap(sb.ofree[d][i]);
+      if (!r) r = swap(sb.dready[d][i]);
+      if (!r) r = swap(sb.cons_r[d][i]);
+      if (!r) r = swap(sb.cons_o[d][i]);
+    }
+    for (auto& e : c->ch[d].sent_ev) if (!r) r = swap(e);
+    for (auto& e : c->ch[d].recvd_ev) if (!r) r = swap(e);
+  }
+  return r;
+}
 
 void reset_step_state(ppc_comm* c) {
   StepBufs& sb = c->sb;
@@ -79,6 +105,8 @@ ppc_status_t ppc_graph_create(ppc_comm_t* const* comms, int n, const ppc_step_t*
       c->capturing = false;
       c->cfg.trace = saved_trace[k];
       reset_step_state(c);
+      DeviceGuard dgk(c->device);
+      if (swap_events(c, g->captured) != cudaSuccess && !st) st = PPC_ERR_CUDA;
     }
     return st;
   };
@@ -115,7 +143,7 @@ ppc_status_t ppc_graph_create(ppc_comm_t* const* comms, int n, const ppc_step_t*
   if (!st && ec != cudaSuccess) st = PPC_ERR_CUDA;
   if (fork) cudaEventDestroy(fork);
   for (cudaEvent_t e : joins) if (e) cudaEventDestroy(e);
-  finish(st);
+  st = finish(st);
   if (!st) {
     const cudaError_t ei = cudaGraphInstantiate(&g->exec, graph, 0);
     if (ei != cudaSuccess) {
@@ -182,6 +210,7 @@ ppc_status_t ppc_graph_destroy(ppc_graph_t* g) {
   if (g->exec) cudaGraphExecDestroy(g->exec);
   if (g->graph) cudaGraphDestroy(g->graph);
   for (cudaEvent_t e : g->ev) if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : g->captured) if (e) cudaEventDestroy(e);
   delete g;
   return PPC_OK;
 }
