@@ -2,15 +2,21 @@
 // sequence numbers relative to per-comm device counters (SeqRef in ppc_internal.h); each
 // launch sets the counters to the host's current sequence numbers, replays the graph and
 // advances the host counters by the step's message counts.
+//
+// The step is captured on private per-stage streams (any caller stream works, including the
+// legacy default stream, which cannot be captured): a launch orders the private streams
+// after the caller's streams and the caller's streams after the replay.
 #include <vector>
 
 #include "ppc_comm_impl.h"
 
 struct ppc_graph {
   std::vector<ppc_comm*> comms;
-  std::vector<cudaStream_t> streams;
+  std::vector<cudaStream_t> user;                 // caller streams, one per stage
+  std::vector<cudaStream_t> cap;                  // private capture / launch streams
   std::vector<uint64_t> dsend[2], drecv[2];       // per comm, messages per step
-  std::vector<cudaEvent_t> ev;                    // prologue joins
+  std::vector<cudaEvent_t> ev_in, ev_pro;         // caller -> launch, prologue joins
+  cudaEvent_t ev_out = nullptr;                   // launch -> callers
   std::vector<cudaEvent_t> captured;              // events referenced by the graph's nodes
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -53,6 +59,14 @@ void reset_step_state(ppc_comm* c) {
     }
 }
 
+cudaEvent_t new_event() {
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+  return e;
+}
+
+#define GDBG(...) do { if (getenv("PPC_DEBUG")) fprintf(stderr, __VA_ARGS__); } while (0)
+
 }  // namespace
 
 extern "C" {
@@ -73,17 +87,32 @@ ppc_status_t ppc_graph_create(ppc_comm_t* const* comms, int n, const ppc_step_t*
   if (n == 1 && comms[0]->local_mode && comms[0]->cfg.pp > 1) return PPC_ERR_INVALID_ARG;
   ppc_graph* g = new ppc_graph();
   g->comms.assign(comms, comms + n);
-  g->streams.assign(streams, streams + n);
-  std::vector<int> saved_trace(n);
-  // quiesce: eager work must not be referenced from inside the capture
+  g->user.assign(streams, streams + n);
+  auto fail = [&](ppc_status_t st) {
+    ppc_graph_destroy(g);
+    return st;
+  };
+  // private streams and events; quiesce: eager work must not be referenced by the capture
   for (int k = 0; k < n; ++k) {
     ppc_comm* c = comms[k];
     DeviceGuard dg(c->device);
-    if (cudaDeviceSynchronize() != cudaSuccess) { delete g; return PPC_ERR_CUDA; }
-    if (!c->dseq && cudaMalloc(&c->dseq, 4 * sizeof(uint64_t)) != cudaSuccess) {
-      delete g;
-      return PPC_ERR_CUDA;
-    }
+    cudaStream_t s = nullptr;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return fail(PPC_ERR_CUDA);
+    g->cap.push_back(s);
+    g->ev_in.push_back(new_event());
+    g->ev_pro.push_back(new_event());
+    if (!g->ev_in.back() || !g->ev_pro.back()) return fail(PPC_ERR_CUDA);
+    if (cudaDeviceSynchronize() != cudaSuccess) return fail(PPC_ERR_CUDA);
+    if (!c->dseq && cudaMalloc(&c->dseq, 4 * sizeof(uint64_t)) != cudaSuccess)
+      return fail(PPC_ERR_CUDA);
+  }
+  {
+    DeviceGuard dg(comms[0]->device);
+    if (!(g->ev_out = new_event())) return fail(PPC_ERR_CUDA);
+  }
+  std::vector<int> saved_trace(n);
+  for (int k = 0; k < n; ++k) {
+    ppc_comm* c = comms[k];
     reset_step_state(c);
     saved_trace[k] = c->cfg.trace;
     c->cfg.trace = 0;                         // no per-launch events / records in the graph
@@ -91,8 +120,8 @@ ppc_status_t ppc_graph_create(ppc_comm_t* const* comms, int n, const ppc_step_t*
       c->cap_send[d] = c->ch[d].send_seq;
       c->cap_recv[d] = c->ch[d].recv_seq;
     }
+    c->capturing = true;
   }
-  for (int k = 0; k < n; ++k) comms[k]->capturing = true;
   auto finish = [&](ppc_status_t st) {
     for (int k = 0; k < n; ++k) {
       ppc_comm* c = comms[k];
@@ -111,60 +140,46 @@ ppc_status_t ppc_graph_create(ppc_comm_t* const* comms, int n, const ppc_step_t*
     return st;
   };
   DeviceGuard dg0(comms[0]->device);
-  cudaStream_t s0 = streams[0];
-  if (cudaStreamBeginCapture(s0, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+  cudaStream_t s0 = g->cap[0];
+  cudaError_t e = cudaStreamBeginCapture(s0, cudaStreamCaptureModeRelaxed);
+  if (e != cudaSuccess) {
+    GDBG("ppc: graph begin capture %s\n", cudaGetErrorString(e));
     finish(PPC_ERR_CUDA);
-    delete g;
-    return PPC_ERR_CUDA;
+    return fail(PPC_ERR_CUDA);
   }
   ppc_status_t st = PPC_OK;
-  // fork every stage stream into the capture
-  cudaEvent_t fork = nullptr;
-  if (cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventRecord(fork, s0) != cudaSuccess)
-    st = PPC_ERR_CUDA;
+  cudaEvent_t fork = new_event();             // fork every stage stream into the capture
+  if (!fork || cudaEventRecord(fork, s0) != cudaSuccess) st = PPC_ERR_CUDA;
   for (int k = 1; k < n && !st; ++k)
-    if (cudaStreamWaitEvent(streams[k], fork, 0) != cudaSuccess) st = PPC_ERR_CUDA;
+    if (cudaStreamWaitEvent(g->cap[k], fork, 0) != cudaSuccess) st = PPC_ERR_CUDA;
   if (!st) st = n == 1 ? ppc_step_1f1b(comms[0], &steps[0], s0)
-                       : ppc_step_1f1b_local(comms, n, steps, streams);
-  // join them back
-  std::vector<cudaEvent_t> joins(n, nullptr);
+                       : ppc_step_1f1b_local(comms, n, steps, g->cap.data());
+  if (st) GDBG("ppc: graph capture of the step failed: %d\n", (int)st);
+  std::vector<cudaEvent_t> joins(n, nullptr);  // join them back
   for (int k = 1; k < n && !st; ++k) {
     DeviceGuard dg(comms[k]->device);
-    if (cudaEventCreateWithFlags(&joins[k], cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventRecord(joins[k], streams[k]) != cudaSuccess ||
+    if (!(joins[k] = new_event()) || cudaEventRecord(joins[k], g->cap[k]) != cudaSuccess ||
         cudaStreamWaitEvent(s0, joins[k], 0) != cudaSuccess)
       st = PPC_ERR_CUDA;
   }
   cudaGraph_t graph = nullptr;
-  const cudaError_t ec = cudaStreamEndCapture(s0, &graph);
-  if (getenv("PPC_DEBUG") && (st || ec != cudaSuccess))
-    fprintf(stderr, "ppc: graph capture step=%d end=%s\n", (int)st, cudaGetErrorString(ec));
-  if (!st && ec != cudaSuccess) st = PPC_ERR_CUDA;
+  e = cudaStreamEndCapture(s0, &graph);
+  if (e != cudaSuccess) GDBG("ppc: graph end capture %s\n", cudaGetErrorString(e));
+  if (!st && e != cudaSuccess) st = PPC_ERR_CUDA;
   if (fork) cudaEventDestroy(fork);
-  for (cudaEvent_t e : joins) if (e) cudaEventDestroy(e);
+  for (cudaEvent_t j : joins) if (j) cudaEventDestroy(j);
   st = finish(st);
+  g->graph = graph;
   if (!st) {
-    const cudaError_t ei = cudaGraphInstantiate(&g->exec, graph, 0);
-    if (ei != cudaSuccess) {
-      if (getenv("PPC_DEBUG")) fprintf(stderr, "ppc: graph instantiate %s\n", cudaGetErrorString(ei));
+    e = cudaGraphInstantiate(&g->exec, graph, 0);
+    if (e != cudaSuccess) {
+      GDBG("ppc: graph instantiate %s\n", cudaGetErrorString(e));
       st = PPC_ERR_CUDA;
     }
   }
-  g->graph = graph;
   if (st) {
     cudaGetLastError();
-    ppc_graph_destroy(g);
-    return st;
-  }
-  for (int k = 0; k < n; ++k) {
-    cudaEvent_t e = nullptr;
-    DeviceGuard dg(comms[k]->device);
-    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
-      ppc_graph_destroy(g);
-      return PPC_ERR_CUDA;
-    }
-    g->ev.push_back(e);
+    return fail(st);
   }
   *out = g;
   return PPC_OK;
@@ -177,40 +192,50 @@ ppc_status_t ppc_graph_launch(ppc_graph_t* g) {
     ppc_status_t st = check_live(g->comms[k]);
     if (st) return st;
   }
-  // prologue: every comm's device sequence bases = its host counters, ordered before s0
+  // prologue on the private streams: after the caller's work, set the device sequence
+  // bases of every comm to its host counters, all joined into cap[0]
   for (int k = 0; k < n; ++k) {
     ppc_comm* c = g->comms[k];
     DeviceGuard dg(c->device);
+    CK(cudaEventRecord(g->ev_in[k], g->user[k]));
+    CK(cudaStreamWaitEvent(g->cap[k], g->ev_in[k], 0));
     CK(launch_set_seq(c->dseq, c->ch[0].send_seq, c->ch[1].send_seq, c->ch[0].recv_seq,
-                      c->ch[1].recv_seq, g->streams[k]));
+                      c->ch[1].recv_seq, g->cap[k]));
     if (k > 0) {
-      CK(cudaEventRecord(g->ev[k], g->streams[k]));
+      CK(cudaEventRecord(g->ev_pro[k], g->cap[k]));
       DeviceGuard d0(g->comms[0]->device);
-      CK(cudaStreamWaitEvent(g->streams[0], g->ev[k], 0));
+      CK(cudaStreamWaitEvent(g->cap[0], g->ev_pro[k], 0));
     }
   }
   {
     DeviceGuard d0(g->comms[0]->device);
-    CK(cudaGraphLaunch(g->exec, g->streams[0]));
+    CK(cudaGraphLaunch(g->exec, g->cap[0]));
+    CK(cudaEventRecord(g->ev_out, g->cap[0]));
   }
-  for (int k = 0; k < n; ++k)
+  for (int k = 0; k < n; ++k) {                 // the caller's streams continue after it
+    DeviceGuard dg(g->comms[k]->device);
+    CK(cudaStreamWaitEvent(g->user[k], g->ev_out, 0));
     for (int d = 0; d < 2; ++d) {
       g->comms[k]->ch[d].send_seq += g->dsend[d][k];
       g->comms[k]->ch[d].recv_seq += g->drecv[d][k];
     }
+  }
   return PPC_OK;
 }
 
 ppc_status_t ppc_graph_destroy(ppc_graph_t* g) {
   if (!g) return PPC_ERR_INVALID_ARG;
-  if (!g->comms.empty()) {
-    DeviceGuard dg(g->comms[0]->device);
+  for (ppc_comm* c : g->comms) {
+    DeviceGuard dg(c->device);
     cudaDeviceSynchronize();
   }
   if (g->exec) cudaGraphExecDestroy(g->exec);
   if (g->graph) cudaGraphDestroy(g->graph);
-  for (cudaEvent_t e : g->ev) if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : g->ev_in) if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : g->ev_pro) if (e) cudaEventDestroy(e);
+  if (g->ev_out) cudaEventDestroy(g->ev_out);
   for (cudaEvent_t e : g->captured) if (e) cudaEventDestroy(e);
+  for (cudaStream_t s : g->cap) if (s) cudaStreamDestroy(s);
   delete g;
   return PPC_OK;
 }
