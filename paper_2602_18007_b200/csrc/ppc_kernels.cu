@@ -394,6 +394,8 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(RecvArgs a0) {
           fail = 1;
         } else {
           s_zc_src = reinterpret_cast<const uint8_t*>(base + h->src_off);
+          // trace: a zero-copy receive starts moving data when the publication is seen
+          if (a.rec && blockIdx.x == 0) a.rec->t_start_ns = (long long)globaltimer();
         }
       }
     }

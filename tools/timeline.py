@@ -20,6 +20,7 @@ ap.add_argument("--chunk", type=int, default=1 << 20)
 ap.add_argument("--cta", type=int, default=0)
 ap.add_argument("--M", type=int, default=8)
 ap.add_argument("--out", default="gpurun_out/timeline")
+ap.add_argument("--zc", type=int, default=0)
 a = ap.parse_args()
 rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
 torch.cuda.set_device(rank)
@@ -36,6 +37,8 @@ OUT = [torch.empty(n, dtype=torch.uint8, device="cuda") for _ in range(M)]
 sa = ppc.StepArgs(M, n, n, x=X, g=G, y=OUT if rank == world - 1 else None,
                   dx=OUT if rank == 0 else None)
 s = torch.cuda.current_stream()
+if a.zc:
+    ppc.register_tensors(comm, X or G)
 for _ in range(3):
     ppc.step_1f1b(comm, sa, s)
 torch.cuda.synchronize()
