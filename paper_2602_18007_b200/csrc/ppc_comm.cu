@@ -350,8 +350,20 @@ ppc_status_t ppc_group(const ppc_comm_t* c, ppc_group_t g, int* members, int* n,
   return PPC_OK;
 }
 
+int ppc_impl_is_zero_copy(const ppc_comm_t* c, const void* buf, size_t bytes) {
+  uint64_t off = 0;
+  return c && !c->local_mode && bytes > 0 && buf && find_reg(c, buf, bytes, &off) >= 0;
+}
+
 ppc_status_t ppc_pp_send(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_t bytes,
                          long long mb, cudaStream_t s) {
+  return ppc_impl_send_ex(c, d, buf, bytes, mb, s, s);
+}
+
+// s: the data mover / publication; s_wait: the zero-copy rendezvous wait (the step driver
+// publishes on the compute stream and waits for consumption on the send stream)
+ppc_status_t ppc_impl_send_ex(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_t bytes,
+                              long long mb, cudaStream_t s, cudaStream_t s_wait) {
   ppc_status_t st = check_live(c);
   if (st) return st;
   if (d != PPC_FWD && d != PPC_BWD) return PPC_ERR_INVALID_ARG;
@@ -384,6 +396,7 @@ ppc_status_t ppc_pp_send(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_t byt
   uint64_t zc_off = 0;
   const int zc_seg = (!c->local_mode && bytes > 0) ? find_reg(c, buf, bytes, &zc_off) : -1;
   if (zc_seg >= 0) {              // registered buffer: publish it, the receiver pulls it
+    if (rec) --c->trace_n;        // the receiver's record times the transfer
     PublishArgs p{};
     p.hdr = h.o_hdr + slot;
     p.hdr_flag = h.o_hdr_flag + slot;
@@ -408,7 +421,12 @@ ppc_status_t ppc_pp_send(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_t byt
       p.hdr_flag = h.o_hdr_flag;
     }
     CK(launch_publish(p, s));
-    CK(launch_wait_credit(h.credit, target, c->err_dev, c->timeout_ns, s, base));   // rendezvous
+    if (s_wait != s) {
+      if (!c->zc_ev[d]) CK(cudaEventCreateWithFlags(&c->zc_ev[d], cudaEventDisableTiming));
+      CK(cudaEventRecord(c->zc_ev[d], s));
+      CK(cudaStreamWaitEvent(s_wait, c->zc_ev[d], 0));
+    }
+    CK(launch_wait_credit(h.credit, target, c->err_dev, c->timeout_ns, s_wait, base));  // rendezvous
   } else if (c->cfg.engine != PPC_ENGINE_CE || bytes == 0) {  // SM push, or PULL's staging
     PushArgs a{};
     a.src = static_cast<const uint8_t*>(buf);
@@ -778,6 +796,7 @@ ppc_status_t ppc_destroy(ppc_comm_t* c) {
     if (c->hx_buf) cudaFree(c->hx_buf);
     if (c->seg_tab) cudaFree(c->seg_tab);
     if (c->dseq) cudaFree(c->dseq);
+    for (int d = 0; d < 2; ++d) if (c->zc_ev[d]) cudaEventDestroy(c->zc_ev[d]);
     if (c->arena) cudaFree(c->arena);
     if (c->err_host) cudaFreeHost(c->err_host);
   }

@@ -143,11 +143,19 @@ struct ppc_comm {
   // CUDA-graph capture (ppc_graph_create): sends / receives enqueued while capturing use
   // sequence numbers relative to cap_*; dseq = {send FWD, send BWD, recv FWD, recv BWD}
   // device bases, set before each graph launch
+  cudaEvent_t zc_ev[2] = {nullptr, nullptr};   // publication -> rendezvous-wait stream
   bool capturing = false;
   uint64_t cap_send[2] = {0, 0}, cap_recv[2] = {0, 0};
   uint64_t* dseq = nullptr;
   Blob blob{};
 };
+
+// internal entry points shared by the host translation units (not in the C ABI header)
+extern "C" {
+ppc_status_t ppc_impl_send_ex(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_t bytes,
+                              long long mb, cudaStream_t s, cudaStream_t s_wait);
+int ppc_impl_is_zero_copy(const ppc_comm_t* c, const void* buf, size_t bytes);
+}
 
 namespace ppc_impl {
 

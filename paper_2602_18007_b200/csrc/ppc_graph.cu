@@ -43,6 +43,7 @@ cudaError_t swap_events(ppc_comm* c, std::vector<cudaEvent_t>& keep) {
       if (!r) r = swap(sb.cons_r[d][i]);
       if (!r) r = swap(sb.cons_o[d][i]);
     }
+    if (!r) r = swap(c->zc_ev[d]);
     for (auto& e : c->ch[d].sent_ev) if (!r) r = swap(e);
     for (auto& e : c->ch[d].recvd_ev) if (!r) r = swap(e);
   }

@@ -83,6 +83,7 @@ struct Stepper {
   bool* send_pending = nullptr;
   int send_buf = 0;             // direct mode: 0 = user buffer, 1 = rbuf, 2 = obuf
   bool direct = false;          // the receive landed in the terminal destination already
+  bool zc_send = false;         // this op's send source is a registered buffer
   // direct mode: inbox[d] = messages sent to this stage in direction d; out[d] = receiver's
   Mailbox* inbox[2] = {nullptr, nullptr};
   Mailbox* outbox[2] = {nullptr, nullptr};
@@ -210,7 +211,10 @@ struct Stepper {
             send_pending = nullptr;
             send_buf = 0;
           }
-          if (!dmode) {
+          // zero-copy sends publish straight from the compute stream (no cross-stream hop on
+          // the critical path) and wait for consumption on the send stream
+          zc_send = !dmode && ppc_impl_is_zero_copy(c, send_src, bytes);
+          if (!dmode && !zc_send) {
             CK(cudaEventRecord(sb.ready, cs));
             CK(cudaStreamWaitEvent(c->side[d], sb.ready, 0));
           }
@@ -256,7 +260,9 @@ struct Stepper {
             if (p.held) *p.held = true;
             outbox[d]->push_back(p);
           } else {
-            ppc_status_t ss = ppc_pp_send(c, (ppc_dir_t)d, send_src, bytes, m, c->side[d]);
+            ppc_status_t ss = zc_send
+                ? ppc_impl_send_ex(c, (ppc_dir_t)d, send_src, bytes, m, cs, c->side[d])
+                : ppc_pp_send(c, (ppc_dir_t)d, send_src, bytes, m, c->side[d]);
             if (ss == PPC_ERR_WOULD_BLOCK) return PPC_OK;
             if (ss) return ss;
             if (send_free) {
