@@ -494,7 +494,8 @@ ppc_status_t ppc_impl_send_ex(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_
       CK(cudaStreamWaitEvent(s, c->ce_join[i], 0));
     }
   }
-  if (ppc_status_t ts = time_mark(c, 0, s, false)) return ts;
+  // zero-copy: the send completes when the receiver has pulled it (on s_wait)
+  if (ppc_status_t ts = time_mark(c, 0, zc_seg >= 0 ? s_wait : s, false)) return ts;
   h.send_seq = seq;
   if (c->local_mode) CK(cudaEventRecord(h.sent_ev[slot], s));
   return PPC_OK;

@@ -283,6 +283,45 @@ def case_graph(rank, world, zc=False):
     return comm
 
 
+def case_fullsize(rank, world):
+    """BASELINE.json full sizes in bench.py's launch configuration (zero-copy registered
+    sends, 256 KiB grain, the step replayed as a CUDA graph): 2 ranks = C2 (LLaMA-8B-shaped
+    [1,4096,4096] bf16, PP=2, M=8); 4 ranks = C4 stand-in (Qwen2-7B-shaped [1,4096,3584],
+    PP=4, M=32).  Identity stages: the last stage must hold X_m, stage 0 G_m, byte for byte;
+    micro-batches 0, 1 and M-1 are compared (sampled), every step of 3 graph launches."""
+    S = world
+    hidden, M = (4096, 8) if world == 2 else (3584, 32)
+    n = 4096 * hidden * 2
+    cfg = ppc.make_config(pp=S, max_msg_bytes=n, chunk_bytes=256 << 10)
+    comm = ppc.connect_distributed(cfg, rank, world, rank, with_nccl=False)
+    s = torch.cuda.Stream()
+    X = [buf(n) for _ in range(M)] if rank == 0 else None
+    G = [buf(n) for _ in range(M)] if rank == S - 1 else None
+    out = [buf(n) for _ in range(M)] if rank in (0, S - 1) else None
+    for m in range(M):
+        if X:
+            ppc.fill_payload(X[m], n, 42, 0, P.SRC_BOUNDARY, 0, m)
+        if G:
+            ppc.fill_payload(G[m], n, 42, 0, P.SRC_BOUNDARY, 1, m)
+    ppc.register_tensors(comm, X or G or [])
+    args = ppc.StepArgs(M, n, n, x=X, g=G, y=out if rank == S - 1 else None,
+                        dx=out if rank == 0 else None)
+    ppc.step_1f1b(comm, args, s)
+    torch.cuda.synchronize()
+    graph = ppc.StepGraph([comm], [args], [s])
+    for _ in range(3):
+        graph.launch()
+        torch.cuda.synchronize()
+        assert comm.poll() == 0
+        if out:
+            for m in (0, 1, M - 1):
+                ref = P.source_gradient(42, 0, m, n) if rank == 0 else P.source_activation(42, 0, m, n)
+                assert np.array_equal(host(out[m]), ref), (rank, m)
+                out[m].fill_(0)
+    graph.destroy()
+    return comm
+
+
 def case_hetero(rank, world):
     """NEXT-2: hetero allreduce = NCCL in each stage's DP subgroup + leader exchange over the
     PP path + NCCL broadcast; compared exactly (integer-valued fp32) with the oracle."""
@@ -332,6 +371,8 @@ def main():
         comm = case_zc(rank, world)
     elif case == "graph":
         comm = case_graph(rank, world)
+    elif case == "fullsize":
+        comm = case_fullsize(rank, world)
     elif case == "dcbs":
         comm = case_dcbs(rank, world)
     else:

@@ -52,3 +52,9 @@ def test_zero_copy_registered_pull():
 @pytest.mark.parametrize("n", [2, 4])
 def test_step_cuda_graph(n):
     _run("graph", n)
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_full_size_bench_configuration(n):
+    """C2 (2 GPUs) / C4 stand-in (4 GPUs) at full size in bench.py's launch configuration."""
+    _run("fullsize", n, timeout=600)
