@@ -46,7 +46,7 @@ def parse():
                          "512 KiB ring push, 128 KiB virtual stages)")
     ap.add_argument("--channels", type=int, default=1)
     ap.add_argument("--cta", type=int, default=0)
-    ap.add_argument("--slots", type=int, default=2)
+    ap.add_argument("--slots", type=int, default=0, help="ring slots K; 0 = pp + 1")
     ap.add_argument("--graph", type=int, default=1,
                     help="replay the step as one CUDA graph (ppc_graph_create)")
     ap.add_argument("--zc", type=int, default=1,
@@ -184,7 +184,7 @@ def workload_config(args, pipelines, virtual):
             "pp": args.pp, "pipelines": pipelines, "virtual_stages": virtual, "M": args.M,
             "seq": args.seq, "hidden": args.hidden, "msg_bytes": args.seq * args.hidden * 2,
             "engine": args.engine, "chunk_bytes": args.chunk, "channels": args.channels,
-            "ring_slots": args.slots, "zero_copy_sends": bool(args.zc) and not virtual,
+            "ring_slots": args.slots or args.pp + 1, "zero_copy_sends": bool(args.zc) and not virtual,
             "cuda_graph": bool(args.graph),
             "l2": "inputs larger than L2 (M x 32 MiB per stage per direction, 256 MiB)"}
 

@@ -74,7 +74,8 @@ typedef enum { PPC_BACKEND_NCCL = 0, PPC_BACKEND_PEER = 1, PPC_BACKEND_NONE = 2 
 typedef struct {
   int tp, pp, dp;               /* grid; rank = pp_i*(tp*dp) + dp_i*tp + tp_i */
   size_t max_msg_bytes;         /* ring slot payload capacity                                  */
-  int ring_slots;               /* K; 0 => 2 (double buffering)                        */
+  int ring_slots;               /* K; 0 => pp + 1 (1F1B occupancy bound + 1: sends never wait
+                                   for a slot; SPEC's double buffering is K = 2)        */
   int channels;                 /* MPDT analogue: SM engine = CTA groups, CE engine =
                                    copy streams; 1..8; 0 => 1                                  */
   size_t chunk_bytes;           /* flag granularity, multiple of 4096; 0 => 1 MiB              */

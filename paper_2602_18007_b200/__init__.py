@@ -147,7 +147,7 @@ def _stream(s):
     return s.cuda_stream
 
 
-def make_config(tp=1, pp=2, dp=1, max_msg_bytes=32 << 20, ring_slots=2, channels=1,
+def make_config(tp=1, pp=2, dp=1, max_msg_bytes=32 << 20, ring_slots=0, channels=1,
                 chunk_bytes=1 << 20, engine=ENGINE_SM, cta_per_channel=0, timeout_ns=0,
                 trace=0) -> Config:
     return Config(tp, pp, dp, max_msg_bytes, ring_slots, channels, chunk_bytes, engine,

@@ -133,7 +133,9 @@ ppc_status_t ppc_create(const ppc_config_t* cfg, int world, int rank, int cuda_d
   c->world = world;
   c->rank = rank;
   c->device = cuda_device;
-  c->K = cfg->ring_slots ? cfg->ring_slots : 2;
+  // default K = pp + 1: under 1F1B stage s never has more than min(S - s, M) unconsumed
+  // messages per boundary, so sends never wait for a slot
+  c->K = cfg->ring_slots ? cfg->ring_slots : std::min(cfg->pp + 1, kMaxSlots);
   c->chunk = cfg->chunk_bytes ? cfg->chunk_bytes : (1u << 20);
   c->timeout_ns = cfg->timeout_ns ? cfg->timeout_ns : 10000000000ull;
   if (c->cfg.channels == 0) c->cfg.channels = 1;

@@ -59,6 +59,29 @@ def test_send_recv_bit_exact(K, sizes):
         c.destroy()
 
 
+@pytest.mark.parametrize("engine", [ppc.ENGINE_SM, ppc.ENGINE_CE, ppc.ENGINE_PULL])
+@pytest.mark.parametrize("src_off,dst_off", [(1, 0), (0, 3), (8, 8), (16, 48)])
+def test_misaligned_buffers(engine, src_off, dst_off):
+    """User buffers at byte offsets (16-B vector path, 32-B path, byte fallback) stay exact."""
+    comms = _pair(max_msg_bytes=1 << 20, chunk_bytes=64 << 10, engine=engine)
+    s = torch.cuda.current_stream()
+    for i, n in enumerate([1, 33, 3 * (64 << 10) + 5, (1 << 20) - 64]):
+        src = _buf(n + 64)
+        dst = _buf(n + 64)
+        dst.fill_(0xCD)
+        ppc.fill_payload(src.data_ptr() + src_off, n, 42, 0, 0, 0, i)
+        comms[0].send(ppc.FWD, src.data_ptr() + src_off, n, mb=i, stream=s)
+        comms[1].recv(ppc.FWD, dst.data_ptr() + dst_off, n, mb=i, stream=s)
+        got = _host(dst)
+        assert np.array_equal(got[dst_off:dst_off + n], P.payload_bytes(42, 0, 0, 0, i, n))
+        assert (got[:dst_off] == 0xCD).all() and (got[dst_off + n:] == 0xCD).all()   # no overrun
+    for c in comms:
+        assert c.poll() == 0
+        c.disconnect()
+    for c in comms:
+        c.destroy()
+
+
 def test_would_block_and_header_errors():
     comms = _pair(max_msg_bytes=1 << 20, ring_slots=2, chunk_bytes=64 << 10)
     s = torch.cuda.current_stream()
