@@ -219,7 +219,7 @@ def main():
     cfg = ppc.make_config(tp=1, pp=S, dp=max(1, world // S) if distributed else 1,
                           max_msg_bytes=nbytes, ring_slots=args.slots, channels=args.channels,
                           chunk_bytes=args.chunk, engine=engine, cta_per_channel=args.cta,
-                          trace=2)
+                          trace=3)
     if distributed:
         if world % S:
             raise SystemExit(f"--gpus {world} is not a multiple of pp={S}")
@@ -312,9 +312,13 @@ def main():
     tokens = pipelines * M * args.seq * args.steps
     value = tokens / (ms_total * 1e-3)
     # ---- the same K steps again with per-launch CUDA events for the kernel roofline
+    n_rec0 = [len(c.trace()) for c in comms]
     ms_instr = timed_region(True)
     push_ms = [t for c in comms for t in c.kernel_times(0)]
     recv_ms = [t for c in comms for t in c.kernel_times(1)]
+    # device-side %globaltimer records of the receives of that pass: a zero-copy receive's
+    # record starts when the publication is seen, so t_end - t_start is its pull (data phase)
+    recv_recs = [r for c, n0 in zip(comms, n_rec0) for r in c.trace()[n0:] if r["kind"] == 1]
     for c in comms:
         c.set_trace(0)
     n_launch_local = len(push_ms) + len(recv_ms)
@@ -357,6 +361,13 @@ def main():
                                "note": "this process's transfer launches of the step (both "
                                        "directions, concurrent) over the instrumented step time"},
             "recv_avg_launch_us": (statistics.mean(recv_ms) * 1e3) if recv_ms else None}
+    if distributed and args.zc and recv_recs:
+        phase_us = statistics.mean((r["t_end_ns"] - r["t_start_ns"]) * 1e-3 for r in recv_recs)
+        phase_us = max_over_ranks(phase_us)
+        roof["zero_copy_pull_data_phase"] = {
+            "avg_us": phase_us, "achieved": nbytes / (phase_us * 1e-6) / 1e9, "unit": "GB/s",
+            "frac": nbytes / (phase_us * 1e-6) / 1e9 / peak, "records": len(recv_recs),
+            "timing": "%globaltimer stamps in recv_kernel: publication seen -> last CTA done"}
     boundary_gbps = 2 * M * nbytes * pipelines * (S - 1) * args.steps / (ms_total * 1e-3) / 1e9
 
     # ---- e2e: the same step through the C-ABI with pinned HOST inputs / outputs
