@@ -49,8 +49,11 @@ def parse():
     ap.add_argument("--slots", type=int, default=0, help="ring slots K; 0 = pp + 1")
     ap.add_argument("--graph", type=int, default=1,
                     help="replay the step as one CUDA graph (ppc_graph_create)")
-    ap.add_argument("--zc", type=int, default=1,
-                    help="N>=2: register the step's send buffers (zero-copy NVLink pulls)")
+    ap.add_argument("--zc", type=int, default=-1,
+                    help="N>=2: register the step's send buffers (zero-copy NVLink pulls); "
+                         "-1 = on for pp = 2 (every send is then a pull), off for deeper "
+                         "pipelines (middle stages forward from unregistered buffers and "
+                         "mixing pulls with pushes on one link measured slower)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -208,6 +211,8 @@ def main():
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
+    if args.zc < 0:
+        args.zc = 1 if args.pp == 2 else 0
     if not args.chunk:
         # tuned on 2x B200 (profiles/r1_tune_step_ws.jsonl): 512 KiB chunks x 64 CTAs
         # zero-copy pulls: 256 KiB grain; ring push: 512 KiB (profiles/r11_tune.jsonl)
