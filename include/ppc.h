@@ -179,6 +179,18 @@ ppc_status_t ppc_register(ppc_comm_t* c, const void* ptr, size_t bytes, void* bl
                           size_t* blob_bytes);
 ppc_status_t ppc_register_import(ppc_comm_t* c, const void* blob, size_t blob_bytes);
 
+/* TP-sliced boundary with a fused all-gather (BJ configs[2], PP x TP):
+ * every TP rank of the sending stage sends only its 1/TP slice (ppc_pp_send of slice bytes
+ * from a REGISTERED buffer); every TP rank of the receiving stage calls ppc_pp_recv_gather
+ * with the full size and receives all TP slices, in tp order, pulled over NVLink straight
+ * from the senders' buffers — no separate all-gather.  The receivers of one stage count
+ * their finished pulls in each other's memory; each then returns its own sender's credit,
+ * so a sender reuses its slice only after every receiver pulled it.  Registration blobs of
+ * every rank of the adjacent stage must be imported (ppc_register_import accepts them).
+ * total_bytes must be a multiple of tp.  One process per GPU only. */
+ppc_status_t ppc_pp_recv_gather(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t total_bytes,
+                                long long mb, cudaStream_t s);
+
 /* Pure: the 1F1B op list of stage s (of S) over M micro-batches; ops has room for 2M.
  * w = min(S-s-1, M) forwards, then M-w (F, B) pairs, then w backwards. */
 ppc_status_t ppc_schedule_1f1b(int S, int s, int M, ppc_op_t* ops, int* n_ops);

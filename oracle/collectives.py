@@ -49,5 +49,11 @@ def composed_allreduce(values: Dict[int, np.ndarray], world: int, tp: int, pp: i
     return out
 
 
+def tp_gather_reference(slices):
+    """TP-sliced boundary: the receiving stage's tensor is the
+    concatenation of the sending TP ranks' slices in tp order (an all-gather)."""
+    return np.concatenate([np.asarray(x) for x in slices])
+
+
 def groups_for(world: int, tp: int, pp: int, dp: int):
     return build_groups(world, tp, pp, dp)

@@ -97,6 +97,7 @@ _step = _sig("ppc_step_1f1b", _i, [_vp, C.POINTER(Step), _vp])
 _step_local = _sig("ppc_step_1f1b_local", _i, [C.POINTER(_vp), _i, C.POINTER(Step), C.POINTER(_vp)])
 _allreduce = _sig("ppc_allreduce", _i, [_vp, _i, _vp, _sz, _i, _vp])
 _hx_allreduce = _sig("ppc_hetero_allreduce", _i, [_vp, _vp, _sz, _i, _vp])
+_recv_gather = _sig("ppc_pp_recv_gather", _i, [_vp, _i, _vp, _sz, _ll, _vp])
 _graph_create = _sig("ppc_graph_create", _i, [C.POINTER(_vp), _i, C.POINTER(Step), C.POINTER(_vp),
                                               C.POINTER(_vp)])
 _graph_launch = _sig("ppc_graph_launch", _i, [_vp])
@@ -229,6 +230,12 @@ class Comm:
         p, n = _ptr(tensor)
         _check(_allreduce(self.h, g, p, tensor.numel(), nccl_dtype, _stream(stream)),
                "ppc_allreduce")
+
+    def recv_gather(self, direction, buf, nbytes=None, mb=0, stream=None):
+        """TP-sliced boundary: receive every TP sender's slice (pulled, fused all-gather)."""
+        p, n = _ptr(buf)
+        _check(_recv_gather(self.h, direction, p, n if nbytes is None else nbytes, mb,
+                            _stream(stream)), "ppc_pp_recv_gather")
 
     def register(self, buf, nbytes=None) -> bytes:
         """Register a send buffer for zero-copy pulls; returns the blob for the neighbours."""

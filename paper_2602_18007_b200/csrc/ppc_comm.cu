@@ -292,6 +292,15 @@ ppc_status_t ppc_connect(ppc_comm_t* c, const void* all_blobs, size_t blob_bytes
     uint8_t* base_next = nullptr;
     if (prev >= 0) { ppc_status_t st = map_peer(c, B[prev], &base_prev); if (st) return st; }
     if (next >= 0) { ppc_status_t st = map_peer(c, B[next], &base_next); if (st) return st; }
+    // TP group of this stage: their arenas hold the headers of the slices they receive
+    // (TP-sliced gathers, ppc_pp_recv_gather)
+    c->tp_arena.assign(c->cfg.tp, nullptr);
+    for (int t = 0; t < c->cfg.tp; ++t) {
+      const int r = c->members[PPC_GROUP_TP][t];
+      if (r == c->rank) { c->tp_arena[t] = c->arena; continue; }
+      ppc_status_t st = map_peer(c, B[r], &c->tp_arena[t]);
+      if (st) return st;
+    }
     const Layout& L = c->lay;
     for (int d = 0; d < 2; ++d) {
       Chan& h = c->ch[d];
@@ -541,7 +550,8 @@ ppc_status_t ppc_pp_recv(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t bytes, lo
   a.rec = next_record(c);
   a.rec_src = h.peer_in;
   a.rec_dst = c->rank;
-  a.seg_tab = c->seg_tab ? c->seg_tab + (d == PPC_FWD ? 0 : 1) * kMaxSeg : nullptr;
+  a.seg_tab = c->seg_tab
+      ? c->seg_tab + ((size_t)(d == PPC_FWD ? 0 : 1) * c->cfg.tp + c->tp_i) * kMaxSeg : nullptr;
   if (c->capturing) {             // graph: relative seq, slot resolved on device
     a.sr = {c->dseq + 2 + d, (uint64_t)c->lay.stride, (uint32_t)c->K,
             std::max<uint32_t>(c->lay.max_chunks, 1), 0, 0};
@@ -557,6 +567,55 @@ ppc_status_t ppc_pp_recv(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t bytes, lo
   if (ppc_status_t ts = time_mark(c, 1, s, false)) return ts;
   h.recv_seq = seq;
   if (c->local_mode) CK(cudaEventRecord(h.recvd_ev[slot], s));
+  return PPC_OK;
+}
+
+ppc_status_t ppc_pp_recv_gather(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t total_bytes,
+                                long long mb, cudaStream_t s) {
+  ppc_status_t st = check_live(c);
+  if (st) return st;
+  if (d != PPC_FWD && d != PPC_BWD) return PPC_ERR_INVALID_ARG;
+  const int tp = c->cfg.tp;
+  if (mb < 0 || !buf || total_bytes == 0 || total_bytes % tp != 0 || tp > kMaxTp)
+    return PPC_ERR_INVALID_ARG;
+  Chan& h = c->ch[d];
+  if (h.peer_in < 0) return PPC_ERR_NO_NEIGHBOR;
+  const size_t slice = total_bytes / tp;
+  if (slice > c->cfg.max_msg_bytes) return PPC_ERR_TOO_LARGE;
+  if (c->device < 0 || c->local_mode || c->capturing) return PPC_ERR_STATE;
+  if (!c->seg_tab || (int)c->tp_arena.size() != tp) return PPC_ERR_STATE;   // no imports
+  DeviceGuard g(c->device);
+  const uint64_t seq = h.recv_seq + 1;
+  const int slot = (int)(seq % c->K);
+  const Layout& L = c->lay;
+  const int side = d == PPC_FWD ? 0 : 1;
+  GatherArgs a{};
+  a.dst = static_cast<uint8_t*>(buf);
+  a.slice_bytes = slice;
+  a.chunk = c->chunk;
+  a.n_chunks = (uint32_t)((slice + c->chunk - 1) / c->chunk);
+  a.tp = (uint32_t)tp;
+  a.my_tp = (uint32_t)c->tp_i;
+  a.seq = seq;
+  a.gtarget = (uint64_t)tp * (c->gcount[d] + 1);
+  a.mb = mb;
+  for (int t = 0; t < tp; ++t) {
+    uint8_t* ar = c->tp_arena[t];
+    a.hdr[t] = reinterpret_cast<const SlotHeader*>(ar + L.hdr[d]) + slot;
+    a.hdr_flag[t] = reinterpret_cast<const uint64_t*>(ar + L.hdr_flag[d]) + slot;
+    a.seg_tab[t] = c->seg_tab + ((size_t)side * tp + t) * kMaxSeg;
+    a.gdone[t] = reinterpret_cast<unsigned long long*>(ar + L.gdone[d]);
+  }
+  a.peer_credit = h.peer_credit;
+  a.done = h.i_done + slot;
+  a.err = c->err_dev;
+  a.timeout_ns = c->timeout_ns;
+  const int grid = (int)std::max<uint32_t>(1, std::min<uint32_t>(a.tp * a.n_chunks, 64));
+  if (ppc_status_t ts = time_mark(c, 1, s, true)) return ts;
+  CK(launch_gather(a, grid, s));
+  if (ppc_status_t ts = time_mark(c, 1, s, false)) return ts;
+  h.recv_seq = seq;
+  c->gcount[d] += 1;
   return PPC_OK;
 }
 
@@ -638,13 +697,19 @@ ppc_status_t ppc_register_import(ppc_comm_t* c, const void* blob, size_t blob_by
   if (!c->connected || c->device < 0) return PPC_ERR_STATE;
   RegBlob rb;
   memcpy(&rb, blob, sizeof(rb));
-  if (rb.magic != kRegMagic || rb.seg >= (uint32_t)kMaxSeg) return PPC_ERR_INVALID_ARG;
-  const int side = rb.rank == c->ch[PPC_FWD].peer_in ? 0 : (rb.rank == c->ch[PPC_BWD].peer_in ? 1 : -1);
-  if (side < 0) return PPC_OK;                                   // not a PP neighbour
+  if (rb.magic != kRegMagic || rb.seg >= (uint32_t)kMaxSeg || rb.rank < 0 || rb.rank >= c->world)
+    return PPC_ERR_INVALID_ARG;
+  // senders we may pull from: every rank of an adjacent stage with our dp index (its own PP
+  // neighbour, or a TP peer of it for TP-sliced gathers)
+  const int tp = c->cfg.tp, dp = c->cfg.dp;
+  const int r_pp = rb.rank / (tp * dp), r_dp = (rb.rank % (tp * dp)) / tp, r_tp = rb.rank % tp;
+  const int side = r_dp != c->dp_i ? -1 : (r_pp == c->pp_i - 1 ? 0 : (r_pp == c->pp_i + 1 ? 1 : -1));
+  if (side < 0) return PPC_OK;                                   // not an adjacent stage
   DeviceGuard g(c->device);
+  const size_t tab = (size_t)2 * tp * kMaxSeg * sizeof(uint64_t);
   if (!c->seg_tab) {
-    CK(cudaMalloc(&c->seg_tab, 2 * kMaxSeg * sizeof(uint64_t)));
-    CK(cudaMemset(c->seg_tab, 0, 2 * kMaxSeg * sizeof(uint64_t)));
+    CK(cudaMalloc(&c->seg_tab, tab));
+    CK(cudaMemset(c->seg_tab, 0, tab));
   }
   uint64_t mapped = 0;
   if (rb.pid == c->blob.pid && rb.host_hash == c->blob.host_hash) {
@@ -659,8 +724,8 @@ ppc_status_t ppc_register_import(ppc_comm_t* c, const void* blob, size_t blob_by
     c->reg_opened.push_back(p);
     mapped = (uint64_t)(uintptr_t)p;
   }
-  CK(cudaMemcpy(c->seg_tab + side * kMaxSeg + rb.seg, &mapped, sizeof(mapped),
-                cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->seg_tab + ((size_t)side * tp + r_tp) * kMaxSeg + rb.seg, &mapped,
+                sizeof(mapped), cudaMemcpyHostToDevice));
   return PPC_OK;
 }
 

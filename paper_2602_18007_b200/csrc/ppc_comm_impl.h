@@ -44,7 +44,7 @@ static_assert(sizeof(Blob) == PPC_BLOB_BYTES, "blob size");
 struct Layout {
   size_t stride = 0;             // slot payload stride
   size_t payload[2] = {}, hdr[2] = {}, hdr_flag[2] = {}, flags[2] = {}, credit[2] = {},
-         done[2] = {}, push_done[2] = {};
+         done[2] = {}, push_done[2] = {}, gdone[2] = {};
   size_t total = 0;
   uint32_t max_chunks = 0;
   void build(int K, size_t max_msg, size_t chunk) {
@@ -61,6 +61,8 @@ struct Layout {
     for (int d = 0; d < 2; ++d) { credit[d] = off; off += 256; }
     for (int d = 0; d < 2; ++d) { done[d] = off; off = round_up(off + (size_t)K * 4, 256); }
     for (int d = 0; d < 2; ++d) { push_done[d] = off; off += 256; }
+    // TP-sliced receives: receivers of one stage count finished pulls here (monotone)
+    for (int d = 0; d < 2; ++d) { gdone[d] = off; off += 256; }
     total = round_up(off, kAlign);
   }
 };
@@ -138,12 +140,16 @@ struct ppc_comm {
   // zero-copy registrations: mine (index = segment id) and the neighbours' mapped bases
   struct Reg { uintptr_t base; size_t size; };
   std::vector<Reg> regs;
-  uint64_t* seg_tab = nullptr;    // device [2][kMaxSeg]: 0 = from prev (FWD in), 1 = next
+  // device [2][tp][kMaxSeg]: side 0 = ranks of the previous stage (FWD in), 1 = next stage;
+  // index tp_i of the sending rank (own PP neighbour = own tp_i)
+  uint64_t* seg_tab = nullptr;
   std::vector<void*> reg_opened;
+  std::vector<uint8_t*> tp_arena;   // arenas of this stage's TP group, by tp index (gather)
   // CUDA-graph capture (ppc_graph_create): sends / receives enqueued while capturing use
   // sequence numbers relative to cap_*; dseq = {send FWD, send BWD, recv FWD, recv BWD}
   // device bases, set before each graph launch
   cudaEvent_t zc_ev[2] = {nullptr, nullptr};   // publication -> rendezvous-wait stream
+  uint64_t gcount[2] = {0, 0};                 // TP-sliced gathers received per direction
   bool capturing = false;
   uint64_t cap_send[2] = {0, 0}, cap_recv[2] = {0, 0};
   uint64_t* dseq = nullptr;

@@ -88,6 +88,25 @@ struct RecvArgs {
   const uint64_t* seg_tab;      // zero-copy: mapped bases of the sender's registered buffers
 };
 
+// TP-sliced receive with a fused all-gather (ppc_pp_recv_gather).
+constexpr int kMaxTp = 8;
+struct GatherArgs {
+  uint8_t* dst;
+  uint64_t slice_bytes, chunk;
+  uint32_t n_chunks, tp, my_tp;   // chunks per slice
+  uint64_t seq, gtarget;          // gtarget = tp x gathers so far on this channel
+  int64_t mb;
+  const SlotHeader* hdr[kMaxTp];  // this seq's slot header in receiver t's arena
+  const uint64_t* hdr_flag[kMaxTp];
+  const uint64_t* seg_tab[kMaxTp];
+  unsigned long long* gdone[kMaxTp];   // receiver t's finished-pull counter
+  uint64_t* peer_credit;          // our own sender's credit word
+  uint32_t* done;                 // our slot completion counter
+  ErrWord* err;
+  uint64_t timeout_ns;
+};
+cudaError_t launch_gather(const GatherArgs& a, int grid, cudaStream_t s);
+
 // Zero-copy publication of a registered send buffer: credit wait, header, header flag.
 struct PublishArgs {
   SeqRef sr;

@@ -429,6 +429,68 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(RecvArgs a0) {
   }
 }
 
+// ---------------------------------------------------------------- TP-sliced gather (NEXT-1)
+__global__ void __launch_bounds__(kThreads) gather_kernel(GatherArgs a) {
+  __shared__ const uint8_t* s_src[kMaxTp];
+  uint64_t deadline = 0;
+  int fail = 0;
+  if (threadIdx.x == 0) {
+    deadline = globaltimer() + a.timeout_ns;
+    for (uint32_t t = 0; t < a.tp && !fail; ++t) {
+      if (!wait_geq<true>(a.hdr_flag[t], a.seq, deadline)) {
+        latch(a.err, PPC_ERR_TIMEOUT, a.seq, 0x400u | t << 12);
+        fail = 1;
+        break;
+      }
+      const volatile SlotHeader* h = a.hdr[t];
+      if (h->magic != kMagic || h->seq != a.seq || h->mb != a.mb || !(h->flags & kHdrZeroCopy)) {
+        latch(a.err, PPC_ERR_ORDER, a.seq, 0x400u | t << 12);
+        fail = 1;
+      } else if (h->bytes != a.slice_bytes) {
+        latch(a.err, PPC_ERR_SIZE_MISMATCH, a.seq, 0x400u | t << 12);
+        fail = 1;
+      } else {
+        const uint32_t seg = h->src_seg;
+        const uint64_t base = seg < (uint32_t)kMaxSeg ? a.seg_tab[t][seg] : 0;
+        if (!base) {
+          latch(a.err, PPC_ERR_ORDER, a.seq, 0x500u | t << 12);
+          fail = 1;
+        } else {
+          s_src[t] = reinterpret_cast<const uint8_t*>(base + h->src_off);
+        }
+      }
+    }
+  }
+  if (__syncthreads_or(fail)) return;
+  // every CTA pulls (slice, chunk) units of all TP senders over NVLink into its slot of dst
+  const uint32_t units = a.tp * a.n_chunks;
+  for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
+    const uint32_t t = u / a.n_chunks, c = u % a.n_chunks;
+    const uint64_t off = (uint64_t)c * a.chunk;
+    const uint64_t len = min(a.chunk, a.slice_bytes - off);
+    cta_copy<true>(a.dst + (uint64_t)t * a.slice_bytes + off, s_src[t] + off, len);
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(a.done, 1u) == gridDim.x - 1) {
+    *a.done = 0;
+    __threadfence_system();
+    for (uint32_t t = 0; t < a.tp; ++t) atomicAdd_system(a.gdone[t], 1ull);   // "pulled"
+    // our sender's slice may be reused once every receiver of the stage has pulled it
+    if (!wait_geq<true>(reinterpret_cast<const uint64_t*>(a.gdone[a.my_tp]), a.gtarget,
+                        globaltimer() + a.timeout_ns)) {
+      latch(a.err, PPC_ERR_TIMEOUT, a.seq, 0x600u);
+      return;
+    }
+    st_release_sys(a.peer_credit, a.seq);
+  }
+}
+
+cudaError_t launch_gather(const GatherArgs& a, int grid, cudaStream_t s) {
+  gather_kernel<<<grid, kThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- zero-copy publication
 // The payload stays in the sender's registered buffer; one thread waits for the slot's
 // credit and publishes (segment, offset) in the receiver's slot header.  The stream then

@@ -322,6 +322,40 @@ def case_fullsize(rank, world):
     return comm
 
 
+def case_gather(rank, world):
+    """NEXT-1 TP-sliced boundary with a fused all-gather, PP=2 x TP=2 on 4 GPUs: each TP rank
+    sends only its half of the boundary tensor; each TP rank of the other stage receives the
+    whole tensor (both halves pulled over NVLink).  Compared byte for byte with the oracle's
+    definition (concatenation of the TP slices = the full tensor), both directions, ragged."""
+    from oracle.collectives import tp_gather_reference
+    tp = 2
+    cfg = ppc.make_config(tp=tp, pp=world // tp, dp=1, max_msg_bytes=4 << 20, chunk_bytes=256 << 10)
+    comm = ppc.connect_distributed(cfg, rank, world, rank, with_nccl=False)
+    s = torch.cuda.current_stream()
+    pp_i, tp_i = rank // tp, rank % tp
+    slice_n = 3 * (256 << 10) + 77
+    total = tp * slice_n
+    M = 3
+    fulls = [buf(total) for _ in range(M)]           # what this rank sends slices of
+    d_send = ppc.FWD if pp_i == 0 else ppc.BWD
+    d_recv = ppc.BWD if pp_i == 0 else ppc.FWD
+    for m in range(M):
+        ppc.fill_payload(fulls[m], total, 42, 0, P.SRC_BOUNDARY, d_send, m)
+    ppc.register_tensors(comm, fulls)
+    outs = [buf(total) for _ in range(M)]
+    s_send = torch.cuda.Stream()       # zero-copy sends complete on consumption: own stream
+    for m in range(M):
+        comm.send(d_send, fulls[m].data_ptr() + tp_i * slice_n, slice_n, mb=m, stream=s_send)
+        comm.recv_gather(d_recv, outs[m], total, mb=m, stream=s)
+    torch.cuda.synchronize()
+    assert comm.poll() == 0, ppc.STATUS[comm.poll()]
+    for m in range(M):
+        full = P.payload_bytes(42, 0, P.SRC_BOUNDARY, d_recv, m, total)
+        ref = tp_gather_reference([full[t * slice_n:(t + 1) * slice_n] for t in range(tp)])
+        assert np.array_equal(host(outs[m]), ref), (rank, m)
+    return comm
+
+
 def case_hetero(rank, world):
     """NEXT-2: hetero allreduce = NCCL in each stage's DP subgroup + leader exchange over the
     PP path + NCCL broadcast; compared exactly (integer-valued fp32) with the oracle."""
@@ -373,6 +407,8 @@ def main():
         comm = case_graph(rank, world)
     elif case == "fullsize":
         comm = case_fullsize(rank, world)
+    elif case == "gather":
+        comm = case_gather(rank, world)
     elif case == "dcbs":
         comm = case_dcbs(rank, world)
     else:

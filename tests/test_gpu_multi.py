@@ -58,3 +58,8 @@ def test_step_cuda_graph(n):
 def test_full_size_bench_configuration(n):
     """C2 (2 GPUs) / C4 stand-in (4 GPUs) at full size in bench.py's launch configuration."""
     _run("fullsize", n, timeout=600)
+
+
+def test_tp_sliced_boundary_fused_gather():
+    """NEXT-1 on 4 GPUs (PP=2 x TP=2)."""
+    _run("gather", 4)

@@ -26,3 +26,12 @@ def test_composition_equals_plain_sum(tp, pp, dp):
     for r in range(world):
         group = [q for q in range(world) if q % tp == r % tp]
         assert np.array_equal(out[r], allreduce_reference(vals, group))
+
+
+def test_tp_gather_reference_is_the_inverse_of_slicing():
+    from oracle.collectives import tp_gather_reference
+    full = np.arange(1001, dtype=np.uint8)
+    for tp in (1, 2, 7):
+        n = len(full) // tp * tp
+        parts = [full[i * (n // tp):(i + 1) * (n // tp)] for i in range(tp)]
+        assert np.array_equal(tp_gather_reference(parts), full[:n])
