@@ -238,6 +238,10 @@ ppc_status_t ppc_hetero_allreduce(ppc_comm_t* c, void* buf, size_t count, int nc
 
 /* ---- diagnostics and teardown ---------------------------------------------------------- */
 ppc_status_t ppc_poll(ppc_comm_t* c);              /* non-blocking read of the error word  */
+/* Details of a latched device error: the message seq and where (0x1xx receive header or
+ * chunk wait, 0x2xx credit wait, 0x3xx zero-copy lookup, 0x4xx-0x6xx TP gather; chunk or
+ * tp index in bits 12+; a send's timeout reports its direction). */
+ppc_status_t ppc_error_info(ppc_comm_t* c, unsigned* seq, unsigned* info);
 ppc_status_t ppc_trace(ppc_comm_t* c, ppc_record_t* out, int* n);  /* synchronizes the device;
                                                       *n in: capacity, out: records written */
 /* Device durations (ms) of the send (kind 0) or recv (kind 1) launches enqueued since the

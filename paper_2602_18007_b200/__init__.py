@@ -106,6 +106,7 @@ _register = _sig("ppc_register", _i, [_vp, _vp, _sz, _vp, C.POINTER(_sz)])
 _reg_import = _sig("ppc_register_import", _i, [_vp, _vp, _sz])
 REG_BLOB_BYTES = 128
 _poll = _sig("ppc_poll", _i, [_vp])
+_err_info = _sig("ppc_error_info", _i, [_vp, C.POINTER(C.c_uint), C.POINTER(C.c_uint)])
 _trace = _sig("ppc_trace", _i, [_vp, C.POINTER(Record), C.POINTER(_i)])
 _ktimes = _sig("ppc_kernel_times", _i, [_vp, _i, C.POINTER(C.c_float), C.POINTER(_i)])
 _set_trace = _sig("ppc_set_trace", _i, [_vp, _i])
@@ -257,6 +258,12 @@ class Comm:
 
     def poll(self) -> int:
         return _poll(self.h)
+
+    def error_info(self):
+        """(status name, seq, info) of the latched device error, if any."""
+        seq, info = C.c_uint(0), C.c_uint(0)
+        st = _err_info(self.h, C.byref(seq), C.byref(info))
+        return STATUS[st], seq.value, hex(info.value)
 
     def set_trace(self, trace: int):
         _check(_set_trace(self.h, trace), "ppc_set_trace")

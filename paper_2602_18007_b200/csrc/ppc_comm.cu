@@ -775,6 +775,15 @@ ppc_status_t ppc_hetero_allreduce(ppc_comm_t* c, void* buf, size_t count, int nc
   return PPC_OK;
 }
 
+ppc_status_t ppc_error_info(ppc_comm_t* c, unsigned* seq, unsigned* info) {
+  if (!c || !seq || !info) return PPC_ERR_INVALID_ARG;
+  if (!c->err_host) { *seq = *info = 0; return PPC_OK; }
+  const volatile ErrWord* e = c->err_host;
+  *seq = e->seq;
+  *info = e->info;
+  return (ppc_status_t)e->code;
+}
+
 ppc_status_t ppc_poll(ppc_comm_t* c) {
   if (!c) return PPC_ERR_INVALID_ARG;
   if (!c->err_host) return PPC_OK;

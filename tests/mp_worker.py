@@ -348,7 +348,7 @@ def case_gather(rank, world):
         comm.send(d_send, fulls[m].data_ptr() + tp_i * slice_n, slice_n, mb=m, stream=s_send)
         comm.recv_gather(d_recv, outs[m], total, mb=m, stream=s)
     torch.cuda.synchronize()
-    assert comm.poll() == 0, ppc.STATUS[comm.poll()]
+    assert comm.poll() == 0, comm.error_info()
     for m in range(M):
         full = P.payload_bytes(42, 0, P.SRC_BOUNDARY, d_recv, m, total)
         ref = tp_gather_reference([full[t * slice_n:(t + 1) * slice_n] for t in range(tp)])
