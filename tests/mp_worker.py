@@ -343,7 +343,10 @@ def case_gather(rank, world):
         ppc.fill_payload(fulls[m], total, 42, 0, P.SRC_BOUNDARY, d_send, m)
     ppc.register_tensors(comm, fulls)
     outs = [buf(total) for _ in range(M)]
-    s_send = torch.cuda.Stream()       # zero-copy sends complete on consumption: own stream
+    # zero-copy sends complete on consumption: sends and gathers on two non-default streams
+    # (the legacy default stream would serialise the gather behind the pending send)
+    s_send = torch.cuda.Stream()
+    s = torch.cuda.Stream()
     for m in range(M):
         comm.send(d_send, fulls[m].data_ptr() + tp_i * slice_n, slice_n, mb=m, stream=s_send)
         comm.recv_gather(d_recv, outs[m], total, mb=m, stream=s)
