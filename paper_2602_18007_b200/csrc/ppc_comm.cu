@@ -167,6 +167,7 @@ ppc_status_t ppc_create(const ppc_config_t* cfg, int world, int rank, int cuda_d
     DeviceGuard g(cuda_device);
     auto fail = [&](ppc_status_t st) { ppc_destroy(c); return st; };
     if (cudaSetDevice(cuda_device) != cudaSuccess) return fail(PPC_ERR_CUDA);
+    if (preload_kernels() != cudaSuccess) return fail(PPC_ERR_CUDA);   // no lazy loads later
     if (cudaMalloc(&c->arena, c->lay.total) != cudaSuccess) return fail(PPC_ERR_CUDA);
     if (cudaMemset(c->arena, 0, c->lay.total) != cudaSuccess) return fail(PPC_ERR_CUDA);
     if (cudaHostAlloc(&c->err_host, sizeof(ErrWord), cudaHostAllocMapped) != cudaSuccess)

@@ -157,6 +157,8 @@ cudaError_t launch_add(void* dst, const void* src, size_t count, int dtype, cuda
 // Same-GPU single copy (direct mode of virtual stages): dst <- src, `bytes`, CTA chunks.
 cudaError_t launch_copy(void* dst, const void* src, uint64_t bytes, uint64_t chunk, int grid,
                         cudaStream_t s);
+// load every transport kernel on the current device now (see ppc_kernels.cu)
+cudaError_t preload_kernels();
 // wait until *credit >= target (+ *seq_base when seq_base != nullptr: graph replay)
 cudaError_t launch_wait_credit(const uint64_t* credit, uint64_t target, ErrWord* err,
                                uint64_t timeout_ns, cudaStream_t s,

@@ -646,6 +646,32 @@ cudaError_t launch_ce_flags(uint64_t* flags, uint32_t c0, uint32_t c1, uint64_t 
   return cudaGetLastError();
 }
 
+// Force-load every transport kernel on the current device.  With lazy module loading
+// (CUDA_MODULE_LOADING=LAZY, the CUDA 12 default) the first launch of a kernel loads it,
+// and that load can wait for the device to go idle: a rank whose wait_credit_kernel is
+// spinning on a peer would then block the peer's first receive launch until the wait
+// times out.  Touching the functions up front (cudaFuncGetAttributes loads them) keeps
+// every later launch free of module loads.
+cudaError_t preload_kernels() {
+  cudaFuncAttributes fa;
+  const void* fns[] = {
+      (const void*)push_kernel<true>,      (const void*)push_kernel<false>,
+      (const void*)push_ws_kernel<true>,   (const void*)push_ws_kernel<false>,
+      (const void*)recv_kernel<true>,      (const void*)recv_kernel<false>,
+      (const void*)gather_kernel,          (const void*)publish_kernel,
+      (const void*)ce_head_kernel,         (const void*)ce_flags_kernel,
+      (const void*)wait_credit_kernel,     (const void*)set_seq_kernel,
+      (const void*)add_kernel<float>,      (const void*)add_kernel<__half>,
+      (const void*)add_kernel<__nv_bfloat16>, (const void*)add_kernel<int32_t>,
+      (const void*)copy_kernel,
+  };
+  for (const void* f : fns) {
+    const cudaError_t e = cudaFuncGetAttributes(&fa, f);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 // ---------------------------------------------------------------- K14: test kernels
 // SplitMix64 (synth/payload.py, implemented independently here):
 //   key = seed<<48 ^ step<<32 ^ boundary<<24 ^ dir<<23 ^ mb ; base = mix(key + G)
