@@ -189,7 +189,17 @@ def workload_config(args, pipelines, virtual):
             "engine": args.engine, "chunk_bytes": args.chunk, "channels": args.channels,
             "ring_slots": args.slots or args.pp + 1, "zero_copy_sends": bool(args.zc) and not virtual,
             "cuda_graph": bool(args.graph),
-            "l2": "inputs larger than L2 (M x 32 MiB per stage per direction, 256 MiB)"}
+            "l2": l2_note(args)}
+
+
+def l2_note(args):
+    """How the timing rule on L2 is met: the per-stage working set of one step vs 126 MB L2."""
+    msg = args.seq * args.hidden * 2
+    per_dir = args.M * msg
+    if per_dir > 126 * 10**6:
+        return (f"inputs larger than L2 (M x {msg / 2**20:g} MiB per stage per direction, "
+                f"{per_dir / 2**20:g} MiB)")
+    return f"inputs fit in L2 ({per_dir} B per stage per direction): latency run, not a bench line"
 
 
 # ---------------------------------------------------------------- GPU arm

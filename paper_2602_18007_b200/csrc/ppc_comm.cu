@@ -139,6 +139,8 @@ ppc_status_t ppc_create(const ppc_config_t* cfg, int world, int rank, int cuda_d
   c->chunk = cfg->chunk_bytes ? cfg->chunk_bytes : (1u << 20);
   c->timeout_ns = cfg->timeout_ns ? cfg->timeout_ns : 10000000000ull;
   if (c->cfg.channels == 0) c->cfg.channels = 1;
+  c->zc_side = env_int("PPC_ZC_SIDE", 0) != 0;
+  ppc::g_pdl = env_int("PPC_PDL", 1) != 0 ? 1 : 0;
   const int tp = cfg->tp, dp = cfg->dp;
   c->pp_i = rank / (tp * dp);
   c->dp_i = (rank % (tp * dp)) / tp;
@@ -181,7 +183,8 @@ ppc_status_t ppc_create(const ppc_config_t* cfg, int world, int rank, int cuda_d
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
     for (int d = 0; d < 2; ++d)
-      if (cudaStreamCreateWithPriority(&c->side[d], cudaStreamNonBlocking, hi) != cudaSuccess)
+      if (cudaStreamCreateWithPriority(&c->side[d], cudaStreamNonBlocking, hi) != cudaSuccess ||
+          cudaStreamCreateWithPriority(&c->zcw[d], cudaStreamNonBlocking, hi) != cudaSuccess)
         return fail(PPC_ERR_CUDA);
     if (cfg->engine == PPC_ENGINE_CE) {
       for (int i = 0; i < c->cfg.channels; ++i) {
@@ -373,7 +376,7 @@ ppc_status_t ppc_pp_send(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_t byt
 }
 
 // s: the data mover / publication; s_wait: the zero-copy rendezvous wait (the step driver
-// publishes on the compute stream and waits for consumption on the send stream)
+// publishes on its send stream and waits for consumption on a third stream, ppc_step.cu)
 ppc_status_t ppc_impl_send_ex(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_t bytes,
                               long long mb, cudaStream_t s, cudaStream_t s_wait) {
   ppc_status_t st = check_live(c);
@@ -408,8 +411,10 @@ ppc_status_t ppc_impl_send_ex(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_
   uint64_t zc_off = 0;
   const int zc_seg = (!c->local_mode && bytes > 0) ? find_reg(c, buf, bytes, &zc_off) : -1;
   if (zc_seg >= 0) {              // registered buffer: publish it, the receiver pulls it
-    if (rec) --c->trace_n;        // the receiver's record times the transfer
-    PublishArgs p{};
+    PublishArgs p{};               // the record times the publication; the receiver's the data
+    p.rec = rec;
+    p.rec_src = c->rank;
+    p.rec_dst = h.peer_out;
     p.hdr = h.o_hdr + slot;
     p.hdr_flag = h.o_hdr_flag + slot;
     p.credit = h.credit;
@@ -861,8 +866,14 @@ ppc_status_t ppc_destroy(ppc_comm_t* c) {
         if (sb.ofree[d][i]) cudaEventDestroy(sb.ofree[d][i]);
       }
     if (sb.ready) cudaEventDestroy(sb.ready);
+    if (sb.xgo) cudaEventDestroy(sb.xgo);
+    if (sb.xdone) cudaEventDestroy(sb.xdone);
+    if (sb.xq) cudaStreamDestroy(sb.xq);
     for (int d = 0; d < 2; ++d) if (sb.join[d]) cudaEventDestroy(sb.join[d]);
-    for (int d = 0; d < 2; ++d) if (c->side[d]) cudaStreamDestroy(c->side[d]);
+    for (int d = 0; d < 2; ++d) {
+      if (c->side[d]) cudaStreamDestroy(c->side[d]);
+      if (c->zcw[d]) cudaStreamDestroy(c->zcw[d]);
+    }
     for (int i = 0; i < 8; ++i) {
       if (c->ce[i]) cudaStreamDestroy(c->ce[i]);
       if (c->ce_join[i]) cudaEventDestroy(c->ce_join[i]);

@@ -104,6 +104,10 @@ struct StepBufs {
   // cwait = copy enqueued, wait `cons` before overwriting
   cudaEvent_t dready[2][2] = {}, cons_r[2][2] = {}, cons_o[2][2] = {};
   bool held_r[2][2] = {}, held_o[2][2] = {}, cwait_r[2][2] = {}, cwait_o[2][2] = {};
+  // direct mode, one transfer queue per GPU: xgo = the receiving stage is ready for the
+  // copy (recorded on its stream), xdone = the copy finished (recorded on the queue)
+  cudaEvent_t xgo = nullptr, xdone = nullptr;
+  cudaStream_t xq = nullptr;    // the queue (owned by stage 0's comm; others borrow it)
 };
 
 }  // namespace ppc_impl
@@ -128,6 +132,8 @@ struct ppc_comm {
   ncclComm_t nccl[2] = {nullptr, nullptr};
   std::vector<int> members[3];
   cudaStream_t side[2] = {nullptr, nullptr};   // send streams of the step driver
+  cudaStream_t zcw[2] = {nullptr, nullptr};    // step driver: zero-copy consumption waits
+  bool zc_side = true;                         // step driver publishes zero-copy on side[d]
   cudaStream_t ce[8] = {};                     // CE engine channel streams
   cudaEvent_t ce_fork = nullptr, ce_join[8] = {};
   ppc_record_t* trace_dev = nullptr;

@@ -116,7 +116,7 @@ ppc_status_t ppc_graph_create(ppc_comm_t* const* comms, int n, const ppc_step_t*
     ppc_comm* c = comms[k];
     reset_step_state(c);
     saved_trace[k] = c->cfg.trace;
-    c->cfg.trace = 0;                         // no per-launch events / records in the graph
+    c->cfg.trace &= 1;   // records stay (each replay rewrites them); no per-launch events
     for (int d = 0; d < 2; ++d) {
       c->cap_send[d] = c->ch[d].send_seq;
       c->cap_recv[d] = c->ch[d].recv_seq;

@@ -119,6 +119,8 @@ struct PublishArgs {
   uint32_t src_seg, dir, boundary;
   ErrWord* err;
   uint64_t timeout_ns;
+  ppc_record_t* rec;              // trace: publish kernel entry .. header flag stored
+  int rec_src, rec_dst;
 };
 cudaError_t launch_publish(const PublishArgs& a, cudaStream_t s);
 
@@ -159,6 +161,9 @@ cudaError_t launch_copy(void* dst, const void* src, uint64_t bytes, uint64_t chu
                         cudaStream_t s);
 // load every transport kernel on the current device now (see ppc_kernels.cu)
 cudaError_t preload_kernels();
+// launch transport kernels with programmatic dependent launch (ppc_kernels.cu); set from
+// PPC_PDL by ppc_create
+extern int g_pdl;
 // wait until *credit >= target (+ *seq_base when seq_base != nullptr: graph replay)
 cudaError_t launch_wait_credit(const uint64_t* credit, uint64_t target, ErrWord* err,
                                uint64_t timeout_ns, cudaStream_t s,

@@ -19,6 +19,34 @@
 
 namespace ppc {
 
+int g_pdl = 1;   // programmatic dependent launch for transport kernels (PPC_PDL, ppc_create)
+
+// Programmatic dependent launch (PDL): a transport kernel launched right behind another one
+// on the same stream may be scheduled while its predecessor still runs.  griddepcontrol.wait
+// returns once every prerequisite grid has completed and its memory is visible, so nothing
+// below it can observe a partial predecessor; launch_dependents then lets the NEXT kernel
+// get resident early.  Without the launch attribute both are no-ops.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*k)(KArgs...), unsigned grid, unsigned block, cudaStream_t s,
+                     Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = g_pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -210,6 +238,7 @@ __device__ __forceinline__ PublishArgs resolve(PublishArgs a) {
 // ---------------------------------------------------------------- K9: push (SM engine)
 template <bool kSys>
 __global__ void __launch_bounds__(kThreads) push_kernel(PushArgs a0) {
+  pdl_enter();
   const PushArgs a = resolve(a0);
   uint64_t deadline = 0;
   int fail = 0;
@@ -292,6 +321,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
 
 template <bool kSys>
 __global__ void __launch_bounds__(kWsThreads) push_ws_kernel(PushArgs a0) {
+  pdl_enter();
   const PushArgs a = resolve(a0);
   __shared__ __align__(8) uint64_t full[kWsRing], empty[kWsRing];
   uint64_t deadline = 0;
@@ -365,6 +395,7 @@ __global__ void __launch_bounds__(kWsThreads) push_ws_kernel(PushArgs a0) {
 // ---------------------------------------------------------------- K10: recv + copy-out
 template <bool kSys>
 __global__ void __launch_bounds__(kThreads) recv_kernel(RecvArgs a0) {
+  pdl_enter();
   const RecvArgs a = resolve(a0);
   __shared__ const uint8_t* s_zc_src;   // zero-copy: the sender's buffer, mapped here
   uint64_t deadline = 0;
@@ -431,6 +462,7 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(RecvArgs a0) {
 
 // ---------------------------------------------------------------- TP-sliced gather (NEXT-1)
 __global__ void __launch_bounds__(kThreads) gather_kernel(GatherArgs a) {
+  pdl_enter();
   __shared__ const uint8_t* s_src[kMaxTp];
   uint64_t deadline = 0;
   int fail = 0;
@@ -487,8 +519,7 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(GatherArgs a) {
 }
 
 cudaError_t launch_gather(const GatherArgs& a, int grid, cudaStream_t s) {
-  gather_kernel<<<grid, kThreads, 0, s>>>(a);
-  return cudaGetLastError();
+  return launch_k(gather_kernel, grid, kThreads, s, a);
 }
 
 // ---------------------------------------------------------------- zero-copy publication
@@ -496,6 +527,7 @@ cudaError_t launch_gather(const GatherArgs& a, int grid, cudaStream_t s) {
 // credit and publishes (segment, offset) in the receiver's slot header.  The stream then
 // waits for the receiver's credit (launch_wait_credit) before the buffer may be reused.
 __global__ void publish_kernel(PublishArgs a0) {
+  pdl_enter();
   const PublishArgs a = resolve(a0);
   const uint64_t t0 = globaltimer();
   if (a.need_credit && !wait_geq(a.credit, a.need_credit, t0 + a.timeout_ns)) {
@@ -517,11 +549,14 @@ __global__ void publish_kernel(PublishArgs a0) {
 #pragma unroll
   for (int j = 0; j < 4; ++j) st_data(hd + j, hs[j]);
   st_release_sys(a.hdr_flag, a.seq);   // cumulative: the producer's writes to the buffer too
+  if (a.rec) {
+    fill_record(a.rec, (long long)t0, a.rec_src, a.rec_dst, (int)a.dir, 0, a.seq, a.mb, a.bytes);
+    a.rec->t_end_ns = (long long)globaltimer();
+  }
 }
 
 cudaError_t launch_publish(const PublishArgs& a, cudaStream_t s) {
-  publish_kernel<<<1, 1, 0, s>>>(a);
-  return cudaGetLastError();
+  return launch_k(publish_kernel, 1, 1, s, a);
 }
 
 // ---------------------------------------------------------------- K12: CE signalling
@@ -558,6 +593,7 @@ __global__ void ce_flags_kernel(uint64_t* flags, uint32_t c0, uint32_t c1, uint6
 // Wait until the receiver consumed `target` (credit protocol), bounded.
 __global__ void wait_credit_kernel(const uint64_t* credit, uint64_t target, ErrWord* err,
                                    uint64_t timeout_ns, const uint64_t* seq_base) {
+  pdl_enter();
   if (seq_base) target += *seq_base;
   if (!wait_geq(credit, target, globaltimer() + timeout_ns)) latch(err, PPC_ERR_TIMEOUT, target, 0x200u);
 }
@@ -598,43 +634,58 @@ cudaError_t launch_add(void* dst, const void* src, size_t count, int dtype, cuda
   return cudaGetLastError();
 }
 
-__global__ void __launch_bounds__(kThreads) copy_kernel(uint8_t* dst, const uint8_t* src,
+// K11: same-GPU single copy.  32-B aligned buffers: grid-stride over 32-B vectors with
+// kCopyU predicated loads in flight per thread before their stores, so every size spreads
+// evenly over the grid in one pass (no dependent load->store tail per thread, no partial
+// last wave of chunks); otherwise per-CTA chunks of `chunk` bytes (cta_copy handles any
+// alignment).
+constexpr int kCopyU = 4;
+__global__ void __launch_bounds__(kThreads, 2) copy_kernel(uint8_t* dst, const uint8_t* src,
                                                         uint64_t bytes, uint64_t chunk) {
-  const uint64_t n = (bytes + chunk - 1) / chunk;
-  for (uint64_t c = blockIdx.x; c < n; c += gridDim.x) {
-    const uint64_t off = c * chunk;
-    cta_copy<false>(dst + off, src + off, min(chunk, bytes - off));
+  pdl_enter();
+  if ((((uintptr_t)dst | (uintptr_t)src) & 31) != 0) {
+    const uint64_t n = (bytes + chunk - 1) / chunk;
+    for (uint64_t c = blockIdx.x; c < n; c += gridDim.x) {
+      const uint64_t off = c * chunk;
+      cta_copy<false>(dst + off, src + off, min(chunk, bytes - off));
+    }
+    return;
   }
+  const uint64_t nv = bytes / sizeof(V32);
+  const V32* s = reinterpret_cast<const V32*>(src);
+  V32* d = reinterpret_cast<V32*>(dst);
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (uint64_t b = t; b < nv; b += kCopyU * stride) {
+    V32 v[kCopyU];
+#pragma unroll
+    for (int j = 0; j < kCopyU; ++j)
+      if (b + j * stride < nv) v[j] = ld_src(s + b + j * stride);
+#pragma unroll
+    for (int j = 0; j < kCopyU; ++j)
+      if (b + j * stride < nv) st_data(d + b + j * stride, v[j]);
+  }
+  for (uint64_t k = nv * sizeof(V32) + t; k < bytes; k += stride) dst[k] = src[k];
 }
 
 cudaError_t launch_copy(void* dst, const void* src, uint64_t bytes, uint64_t chunk, int grid,
                         cudaStream_t s) {
   if (bytes == 0) return cudaSuccess;
-  copy_kernel<<<grid, kThreads, 0, s>>>(static_cast<uint8_t*>(dst),
-                                        static_cast<const uint8_t*>(src), bytes, chunk);
-  return cudaGetLastError();
+  return launch_k(copy_kernel, grid, kThreads, s, static_cast<uint8_t*>(dst),
+                  static_cast<const uint8_t*>(src), bytes, chunk);
 }
 
 cudaError_t launch_wait_credit(const uint64_t* credit, uint64_t target, ErrWord* err,
                                uint64_t timeout_ns, cudaStream_t s, const uint64_t* seq_base) {
-  wait_credit_kernel<<<1, 1, 0, s>>>(credit, target, err, timeout_ns, seq_base);
-  return cudaGetLastError();
+  return launch_k(wait_credit_kernel, 1, 1, s, credit, target, err, timeout_ns, seq_base);
 }
 
 cudaError_t launch_push(const PushArgs& a, int grid, bool sys, bool ws, cudaStream_t s) {
-  if (ws) {
-    if (sys) push_ws_kernel<true><<<grid, kWsThreads, 0, s>>>(a);
-    else push_ws_kernel<false><<<grid, kWsThreads, 0, s>>>(a);
-  } else {
-    if (sys) push_kernel<true><<<grid, kThreads, 0, s>>>(a);
-    else push_kernel<false><<<grid, kThreads, 0, s>>>(a);
-  }
-  return cudaGetLastError();
+  if (ws) return launch_k(sys ? push_ws_kernel<true> : push_ws_kernel<false>, grid, kWsThreads, s, a);
+  return launch_k(sys ? push_kernel<true> : push_kernel<false>, grid, kThreads, s, a);
 }
 cudaError_t launch_recv(const RecvArgs& a, int grid, bool sys, cudaStream_t s) {
-  if (sys) recv_kernel<true><<<grid, kThreads, 0, s>>>(a);
-  else recv_kernel<false><<<grid, kThreads, 0, s>>>(a);
-  return cudaGetLastError();
+  return launch_k(sys ? recv_kernel<true> : recv_kernel<false>, grid, kThreads, s, a);
 }
 cudaError_t launch_ce_head(const CeHeadArgs& a, cudaStream_t s) {
   ce_head_kernel<<<1, 1, 0, s>>>(a);

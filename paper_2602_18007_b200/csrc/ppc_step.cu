@@ -28,6 +28,8 @@ ppc_status_t ensure_bufs(ppc_comm* c, size_t bytes) {
   StepBufs& sb = c->sb;
   if (!sb.ready) {
     CK(cudaEventCreateWithFlags(&sb.ready, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&sb.xgo, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&sb.xdone, cudaEventDisableTiming));
     for (int d = 0; d < 2; ++d) {
       CK(cudaEventCreateWithFlags(&sb.join[d], cudaEventDisableTiming));
       for (int i = 0; i < 2; ++i) {
@@ -84,10 +86,13 @@ struct Stepper {
   int send_buf = 0;             // direct mode: 0 = user buffer, 1 = rbuf, 2 = obuf
   bool direct = false;          // the receive landed in the terminal destination already
   bool zc_send = false;         // this op's send source is a registered buffer
+  bool zc_cs = false;           // ... and it is published from the compute stream
+  bool used_zcw[2] = {false, false};
   // direct mode: inbox[d] = messages sent to this stage in direction d; out[d] = receiver's
   Mailbox* inbox[2] = {nullptr, nullptr};
   Mailbox* outbox[2] = {nullptr, nullptr};
   bool dmode = false;
+  cudaStream_t xq = nullptr;    // direct mode: the GPU's transfer queue (nullptr: own stream)
 
   ppc_status_t init(ppc_comm* comm, const ppc_step_t* step, cudaStream_t stream) {
     c = comm;
@@ -146,10 +151,25 @@ struct Stepper {
             if (p.bytes != bytes) return PPC_ERR_SIZE_MISMATCH;
             if (p.mb != m) return PPC_ERR_ORDER;
             box.pop_front();
-            CK(cudaStreamWaitEvent(cs, p.ready, 0));
-            if (ppc_status_t ts = time_mark(c, 0, cs, true)) return ts;
-            CK(launch_copy(r, p.src, bytes, c->chunk, recv_grid(c, (uint32_t)((bytes + c->chunk - 1) / c->chunk)), cs));
-            if (ppc_status_t ts = time_mark(c, 0, cs, false)) return ts;
+            // the copy runs on the GPU's single transfer queue (xq) when there is one:
+            // copies are HBM-bound, so running two at once only splits the bandwidth;
+            // one at a time each gets all of it and the queue order (the round-robin
+            // enqueue order) already respects every dependency
+            cudaStream_t q = xq ? xq : cs;
+            if (xq) {
+              CK(cudaEventRecord(sb.xgo, cs));
+              CK(cudaStreamWaitEvent(xq, sb.xgo, 0));
+            }
+            CK(cudaStreamWaitEvent(q, p.ready, 0));
+            const uint64_t ch = c->chunk;
+            const int grid = env_int("PPC_COPY_CTAS", 296);   // 2 per SM (copy_kernel)
+            if (ppc_status_t ts = time_mark(c, 0, q, true)) return ts;
+            CK(launch_copy(r, p.src, bytes, ch, grid, q));
+            if (ppc_status_t ts = time_mark(c, 0, q, false)) return ts;
+            if (xq) {
+              CK(cudaEventRecord(sb.xdone, xq));
+              CK(cudaStreamWaitEvent(cs, sb.xdone, 0));
+            }
             if (p.consumed) {
               CK(cudaEventRecord(p.consumed, cs));
               *p.held = false;
@@ -211,10 +231,13 @@ struct Stepper {
             send_pending = nullptr;
             send_buf = 0;
           }
-          // zero-copy sends publish straight from the compute stream (no cross-stream hop on
-          // the critical path) and wait for consumption on the send stream
+          // zero-copy sends publish from the send stream by default, so that the next op's
+          // receive kernel is not queued behind the publication on the compute stream (it is
+          // resident and spinning when its header lands); PPC_ZC_SIDE=0 publishes on the
+          // compute stream instead.  Consumption is always awaited on the send stream.
           zc_send = !dmode && ppc_impl_is_zero_copy(c, send_src, bytes);
-          if (!dmode && !zc_send) {
+          zc_cs = zc_send && !c->zc_side;
+          if (!dmode && !zc_cs) {
             CK(cudaEventRecord(sb.ready, cs));
             CK(cudaStreamWaitEvent(c->side[d], sb.ready, 0));
           }
@@ -260,13 +283,16 @@ struct Stepper {
             if (p.held) *p.held = true;
             outbox[d]->push_back(p);
           } else {
-            ppc_status_t ss = zc_send
-                ? ppc_impl_send_ex(c, (ppc_dir_t)d, send_src, bytes, m, cs, c->side[d])
-                : ppc_pp_send(c, (ppc_dir_t)d, send_src, bytes, m, c->side[d]);
+            // zero-copy: the buffer is free once consumed, awaited on zcw[d] off the
+            // publication stream so the next publication is not queued behind it
+            cudaStream_t s_pub = zc_cs ? cs : c->side[d];
+            cudaStream_t s_done = zc_send ? (zc_cs ? c->side[d] : c->zcw[d]) : c->side[d];
+            ppc_status_t ss = ppc_impl_send_ex(c, (ppc_dir_t)d, send_src, bytes, m, s_pub, s_done);
             if (ss == PPC_ERR_WOULD_BLOCK) return PPC_OK;
             if (ss) return ss;
+            if (s_done == c->zcw[d]) used_zcw[d] = true;
             if (send_free) {
-              CK(cudaEventRecord(send_free, c->side[d]));
+              CK(cudaEventRecord(send_free, s_done));
               *send_pending = true;
             }
           }
@@ -287,6 +313,10 @@ struct Stepper {
       if (!(d == 0 ? s < S - 1 : s > 0)) continue;
       CK(cudaEventRecord(c->sb.join[d], c->side[d]));
       CK(cudaStreamWaitEvent(cs, c->sb.join[d], 0));
+      if (used_zcw[d]) {
+        CK(cudaEventRecord(c->sb.join[d], c->zcw[d]));
+        CK(cudaStreamWaitEvent(cs, c->sb.join[d], 0));
+      }
     }
     return PPC_OK;
   }
@@ -329,8 +359,20 @@ extern "C" ppc_status_t ppc_step_1f1b_local(ppc_comm_t* const* comms, int S,
   // mailboxes of the direct (single-copy) mode: box[k][d] = messages into stage k, dir d
   std::vector<Mailbox> box(2 * S);
   const bool dmode = S > 1 && same_device && env_int("PPC_LOCAL_DIRECT", 1) != 0;
+  cudaStream_t xq = nullptr;
+  if (dmode && env_int("PPC_LOCAL_QUEUE", 1) != 0) {
+    ppc_comm* c0 = comms[0];
+    DeviceGuard g(c0->device);
+    if (!c0->sb.xq) {
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      CK(cudaStreamCreateWithPriority(&c0->sb.xq, cudaStreamNonBlocking, hi));
+    }
+    xq = c0->sb.xq;
+  }
   for (int k = 0; k < S && dmode; ++k) {
     sp[k].dmode = true;
+    sp[k].xq = xq;
     sp[k].inbox[0] = &box[2 * k + 0];
     sp[k].inbox[1] = &box[2 * k + 1];
     sp[k].outbox[0] = k + 1 < S ? &box[2 * (k + 1) + 0] : nullptr;

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdint>
 #include <cstdlib>
+#include <string>
 #include <vector>
 #include <cuda_runtime.h>
 
@@ -150,12 +151,109 @@ __global__ void tma_copy(uint8_t* dst, const uint8_t* src, size_t bytes, uint32_
 
 
 
+// Bidirectional mode ("bidir"): GPU0 -> GPU1 and GPU1 -> GPU0 at the same time, as in the
+// steady state of a PP2 1F1B step (F_m+1 and B_m in flight together).  Each direction's
+// mover runs `reps` back-to-back launches on its own stream; GB/s per direction.
+static int bidir() {
+  const size_t maxb = 256ull << 20;
+  uint8_t* a[2];   // a[d]: source of direction d's data, lives on GPU d
+  uint8_t* b[2];   // b[d]: destination of direction d, lives on GPU 1-d
+  for (int d = 0; d < 2; ++d) {
+    CK(cudaSetDevice(d));
+    CK(cudaMalloc(&a[d], maxb)); CK(cudaMemset(a[d], 1 + d, maxb));
+    CK(cudaMalloc(&b[1 - d], maxb)); CK(cudaMemset(b[1 - d], 0, maxb));   // on GPU d
+  }
+  const int tile = 32 << 10, S = 6;
+  for (int d = 0; d < 2; ++d) {
+    CK(cudaSetDevice(d));
+    CK(cudaFuncSetAttribute(tma_copy<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, S * tile));
+  }
+  // mover kinds: 0 = SM load on the receiver, 1 = SM store on the sender, 2 = CE, 3 = TMA load
+  auto launch = [&](int kind, int d, int g, size_t bytes, cudaStream_t* sts) {
+    const int rx = 1 - d;          // receiving GPU of direction d
+    const size_t nv = bytes / 32;
+    uint8_t* out = b[d];       // allocated on GPU rx
+    if (kind == 0) {
+      CK(cudaSetDevice(rx));
+      simt_copy<8, true><<<g, 512, 0, sts[rx]>>>((V32*)out, (const V32*)a[d], nv);
+    } else if (kind == 1) {
+      CK(cudaSetDevice(d));
+      simt_copy<8, false><<<g, 512, 0, sts[d]>>>((V32*)out, (const V32*)a[d], nv);
+    } else if (kind == 2) {
+      CK(cudaSetDevice(d));
+      CK(cudaMemcpyPeerAsync(out, rx, a[d], d, bytes, sts[d]));
+    } else {
+      CK(cudaSetDevice(rx));
+      tma_copy<S><<<g, 32, S * tile, sts[rx]>>>(out, a[d], bytes, tile);
+    }
+  };
+  const char* names[] = {"load", "store", "ce", "tma_load"};
+  // the stream a direction's work runs on: receiver's for pulls, sender's for pushes / CE
+  auto stream_dev = [&](int kind, int d) { return (kind == 0 || kind == 3) ? 1 - d : d; };
+  for (size_t bytes : {32ull << 20, 256ull << 20}) {
+    const int reps = bytes <= (32u << 20) ? 40 : 8;
+    for (int k0 : {0, 1, 2, 3})
+      for (int k1 : {0, 1, 2, 3}) {
+        if (k1 < k0) continue;
+        for (int g : {64, 96, 148}) {
+          if (k0 == 2 && k1 == 2 && g != 64) continue;
+          const int kinds[2] = {k0, k1};
+          // both directions on different devices' streams: if they collide on one device
+          // (e.g. load for d=0 runs on GPU1, store for d=1 runs on GPU1) use two streams
+          cudaStream_t sts2[2][2];
+          for (int d = 0; d < 2; ++d) {
+            CK(cudaSetDevice(d));
+            CK(cudaStreamCreateWithFlags(&sts2[d][0], cudaStreamNonBlocking));
+            CK(cudaStreamCreateWithFlags(&sts2[d][1], cudaStreamNonBlocking));
+          }
+          cudaStream_t use[2][2];   // use[d] = stream array indexed by device for direction d
+          for (int d = 0; d < 2; ++d) { use[d][0] = sts2[0][d]; use[d][1] = sts2[1][d]; }
+          cudaEvent_t e0[2], e1[2];
+          for (int d = 0; d < 2; ++d) {
+            CK(cudaSetDevice(stream_dev(kinds[d], d)));
+            CK(cudaEventCreate(&e0[d])); CK(cudaEventCreate(&e1[d]));
+          }
+          for (int d = 0; d < 2; ++d) launch(kinds[d], d, g, bytes, use[d]);
+          for (int dev = 0; dev < 2; ++dev) { CK(cudaSetDevice(dev)); CK(cudaDeviceSynchronize()); }
+          for (int d = 0; d < 2; ++d) {
+            const int sd = stream_dev(kinds[d], d);
+            CK(cudaSetDevice(sd)); CK(cudaEventRecord(e0[d], use[d][sd]));
+          }
+          for (int r = 0; r < reps; ++r)
+            for (int d = 0; d < 2; ++d) launch(kinds[d], d, g, bytes, use[d]);
+          for (int d = 0; d < 2; ++d) {
+            const int sd = stream_dev(kinds[d], d);
+            CK(cudaSetDevice(sd)); CK(cudaEventRecord(e1[d], use[d][sd]));
+          }
+          double gb[2];
+          for (int d = 0; d < 2; ++d) {
+            CK(cudaEventSynchronize(e1[d]));
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, e0[d], e1[d]));
+            gb[d] = (double)bytes * reps / (ms * 1e-3) / 1e9;
+          }
+          CK(cudaGetLastError());
+          printf("{\"bidir\": \"%s+%s\", \"bytes\": %zu, \"grid\": %d, \"gbps_d0\": %.1f, "
+                 "\"gbps_d1\": %.1f}\n", names[k0], names[k1], bytes, g, gb[0], gb[1]);
+          fflush(stdout);
+          for (int d = 0; d < 2; ++d) {
+            CK(cudaSetDevice(d));
+            cudaStreamDestroy(sts2[d][0]); cudaStreamDestroy(sts2[d][1]);
+            cudaEventDestroy(e0[d]); cudaEventDestroy(e1[d]);
+          }
+        }
+      }
+  }
+  return 0;
+}
+
 int main(int argc, char** argv) {
   int n = 0;
   CK(cudaGetDeviceCount(&n));
   if (n < 2) { printf("{\"error\": \"needs 2 GPUs\"}\n"); return 0; }
   CK(cudaSetDevice(0)); CK(cudaDeviceEnablePeerAccess(1, 0));
   CK(cudaSetDevice(1)); CK(cudaDeviceEnablePeerAccess(0, 0));
+  if (argc > 1 && std::string(argv[1]) == "bidir") return bidir();
   const size_t sizes[] = {32ull << 20, 256ull << 20, 1ull << 30};
   const size_t maxb = 1ull << 30;
   uint8_t *a0, *b1;

@@ -21,6 +21,7 @@ ap.add_argument("--cta", type=int, default=0)
 ap.add_argument("--M", type=int, default=8)
 ap.add_argument("--out", default="gpurun_out/timeline")
 ap.add_argument("--zc", type=int, default=0)
+ap.add_argument("--graph", type=int, default=0, help="time a CUDA-graph replay of the step")
 a = ap.parse_args()
 rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
 torch.cuda.set_device(rank)
@@ -45,9 +46,19 @@ torch.cuda.synchronize()
 dist.barrier()
 n_before = len(comm.trace())
 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-ev0.record(s)
-ppc.step_1f1b(comm, sa, s)
-ev1.record(s)
+if a.graph:   # records captured once; each replay rewrites them
+    sg = ppc.StepGraph([comm], [sa], [s])
+    for _ in range(3):
+        sg.launch()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ev0.record(s)
+    sg.launch()
+    ev1.record(s)
+else:
+    ev0.record(s)
+    ppc.step_1f1b(comm, sa, s)
+    ev1.record(s)
 torch.cuda.synchronize()
 recs = comm.trace()[n_before:]
 out = {"rank": rank, "step_ms": ev0.elapsed_time(ev1), "records": recs}
@@ -62,10 +73,12 @@ if rank == 0:
         for x in d["records"]:
             x["rank"] = r
             allr.append(x)
-    t0 = min(x["t_start_ns"] for x in allr)
-    allr.sort(key=lambda x: x["t_start_ns"])
+    # %globaltimer is per GPU (offsets between GPUs are arbitrary): times are rank-relative
+    t0s = {r: min(x["t_start_ns"] for x in allr if x["rank"] == r) for r in range(world)}
+    allr.sort(key=lambda x: (x["rank"], x["t_start_ns"]))
     print(f"step_ms rank0 {out['step_ms']:.3f}")
     for x in allr:
+        t0 = t0s[x["rank"]]
         print(f"r{x['rank']} {'send' if x['kind'] == 0 else 'recv'} {x['src']}->{x['dst']} seq {x['seq']} "
               f"mb {x['mb']} start {(x['t_start_ns'] - t0) / 1e3:8.1f} us end "
               f"{(x['t_end_ns'] - t0) / 1e3:8.1f} us dur {(x['t_end_ns'] - x['t_start_ns']) / 1e3:6.1f}")
