@@ -223,6 +223,8 @@ def main():
     dev = torch.cuda.current_device()
     if args.zc < 0:
         args.zc = 1 if args.pp == 2 else 0
+    if args.engine == "ce":
+        args.graph = 0        # the CE engine's host-resolved slots are not graph-capturable
     if not args.chunk:
         # tuned on 2x B200 (profiles/r1_tune_step_ws.jsonl): 512 KiB chunks x 64 CTAs
         # zero-copy pulls: 256 KiB grain; ring push: 512 KiB (profiles/r11_tune.jsonl)

@@ -140,6 +140,7 @@ ppc_status_t ppc_create(const ppc_config_t* cfg, int world, int rank, int cuda_d
   c->timeout_ns = cfg->timeout_ns ? cfg->timeout_ns : 10000000000ull;
   if (c->cfg.channels == 0) c->cfg.channels = 1;
   c->zc_side = env_int("PPC_ZC_SIDE", 0) != 0;
+  c->fuse_publish = env_int("PPC_FUSE_PUBLISH", 1) != 0;
   ppc::g_pdl = env_int("PPC_PDL", 1) != 0 ? 1 : 0;
   const int tp = cfg->tp, dp = cfg->dp;
   c->pp_i = rank / (tp * dp);
@@ -370,6 +371,80 @@ int ppc_impl_is_zero_copy(const ppc_comm_t* c, const void* buf, size_t bytes) {
   return c && !c->local_mode && bytes > 0 && buf && find_reg(c, buf, bytes, &off) >= 0;
 }
 
+}  // extern "C"
+
+namespace {
+// Publication of zero-copy send `seq` (the record times the publication; the receiver's
+// record times the data).
+void fill_publish(ppc_comm* c, ppc_dir_t d, uint64_t seq, uint64_t need, size_t bytes,
+                  long long mb, int zc_seg, uint64_t zc_off, ppc_record_t* rec, ZcSend* z) {
+  Chan& h = c->ch[d];
+  const int slot = (int)(seq % c->K);
+  PublishArgs& p = z->p;
+  p = PublishArgs{};
+  p.rec = rec;
+  p.rec_src = c->rank;
+  p.rec_dst = h.peer_out;
+  p.hdr = h.o_hdr + slot;
+  p.hdr_flag = h.o_hdr_flag + slot;
+  p.credit = h.credit;
+  p.need_credit = need;
+  p.bytes = bytes;
+  p.seq = seq;
+  p.src_off = zc_off;
+  p.mb = mb;
+  p.src_seg = (uint32_t)zc_seg;
+  p.dir = d;
+  p.boundary = (uint32_t)(d == PPC_FWD ? c->pp_i : c->pp_i - 1);
+  p.err = c->err_dev;
+  p.timeout_ns = c->timeout_ns;
+  z->d = d;
+  z->base = nullptr;
+  z->target = seq;
+  if (c->capturing) {             // graph: relative seq, slot resolved on device
+    z->base = c->dseq + d;
+    p.sr = {z->base, 0, (uint32_t)c->K, 0, c->local_mode ? 0u : 1u, 0};
+    p.seq = z->target = seq - c->cap_send[d];
+    p.hdr = h.o_hdr;
+    p.hdr_flag = h.o_hdr_flag;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+ppc_status_t ppc_impl_zc_commit(ppc_comm_t* c, const ZcSend& z, cudaStream_t s,
+                                cudaStream_t s_wait) {
+  if (s_wait != s) {
+    if (!c->zc_ev[z.d]) CK(cudaEventCreateWithFlags(&c->zc_ev[z.d], cudaEventDisableTiming));
+    CK(cudaEventRecord(c->zc_ev[z.d], s));
+    CK(cudaStreamWaitEvent(s_wait, c->zc_ev[z.d], 0));
+  }
+  // rendezvous: the buffer may be reused once the receiver consumed it
+  CK(launch_wait_credit(c->ch[z.d].credit, z.target, c->err_dev, c->timeout_ns, s_wait, z.base));
+  return PPC_OK;
+}
+
+ppc_status_t ppc_impl_zc_prepare(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_t bytes,
+                                 long long mb, ZcSend* z) {
+  ppc_status_t st = check_live(c);
+  if (st) return st;
+  if (d != PPC_FWD && d != PPC_BWD) return PPC_ERR_INVALID_ARG;
+  if (mb < 0 || bytes == 0 || !buf || !z) return PPC_ERR_INVALID_ARG;
+  Chan& h = c->ch[d];
+  if (h.peer_out < 0) return PPC_ERR_NO_NEIGHBOR;
+  if (bytes > c->cfg.max_msg_bytes) return PPC_ERR_TOO_LARGE;
+  if (c->device < 0 || c->local_mode) return PPC_ERR_STATE;
+  uint64_t zc_off = 0;
+  const int zc_seg = find_reg(c, buf, bytes, &zc_off);
+  if (zc_seg < 0) return PPC_ERR_INVALID_ARG;
+  const uint64_t seq = h.send_seq + 1;
+  const uint64_t need = seq > (uint64_t)c->K ? seq - c->K : 0;
+  fill_publish(c, d, seq, need, bytes, mb, zc_seg, zc_off, next_record(c), z);
+  h.send_seq = seq;
+  return PPC_OK;
+}
+
 ppc_status_t ppc_pp_send(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_t bytes,
                          long long mb, cudaStream_t s) {
   return ppc_impl_send_ex(c, d, buf, bytes, mb, s, s);
@@ -411,39 +486,10 @@ ppc_status_t ppc_impl_send_ex(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_
   uint64_t zc_off = 0;
   const int zc_seg = (!c->local_mode && bytes > 0) ? find_reg(c, buf, bytes, &zc_off) : -1;
   if (zc_seg >= 0) {              // registered buffer: publish it, the receiver pulls it
-    PublishArgs p{};               // the record times the publication; the receiver's the data
-    p.rec = rec;
-    p.rec_src = c->rank;
-    p.rec_dst = h.peer_out;
-    p.hdr = h.o_hdr + slot;
-    p.hdr_flag = h.o_hdr_flag + slot;
-    p.credit = h.credit;
-    p.need_credit = need;
-    p.bytes = bytes;
-    p.seq = seq;
-    p.src_off = zc_off;
-    p.mb = mb;
-    p.src_seg = (uint32_t)zc_seg;
-    p.dir = d;
-    p.boundary = (uint32_t)boundary;
-    p.err = c->err_dev;
-    p.timeout_ns = c->timeout_ns;
-    const uint64_t* base = nullptr;
-    uint64_t target = seq;
-    if (c->capturing) {           // graph: relative seq, slot resolved on device
-      base = c->dseq + d;
-      p.sr = {base, 0, (uint32_t)c->K, 0, c->local_mode ? 0u : 1u, 0};
-      p.seq = target = seq - c->cap_send[d];
-      p.hdr = h.o_hdr;
-      p.hdr_flag = h.o_hdr_flag;
-    }
-    CK(launch_publish(p, s));
-    if (s_wait != s) {
-      if (!c->zc_ev[d]) CK(cudaEventCreateWithFlags(&c->zc_ev[d], cudaEventDisableTiming));
-      CK(cudaEventRecord(c->zc_ev[d], s));
-      CK(cudaStreamWaitEvent(s_wait, c->zc_ev[d], 0));
-    }
-    CK(launch_wait_credit(h.credit, target, c->err_dev, c->timeout_ns, s_wait, base));  // rendezvous
+    ZcSend z;
+    fill_publish(c, d, seq, need, bytes, mb, zc_seg, zc_off, rec, &z);
+    CK(launch_publish(z.p, s));
+    if (ppc_status_t ws = ppc_impl_zc_commit(c, z, s, s_wait)) return ws;
   } else if (c->cfg.engine != PPC_ENGINE_CE || bytes == 0) {  // SM push, or PULL's staging
     PushArgs a{};
     a.src = static_cast<const uint8_t*>(buf);
@@ -520,6 +566,13 @@ ppc_status_t ppc_impl_send_ex(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_
 
 ppc_status_t ppc_pp_recv(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t bytes, long long mb,
                          cudaStream_t s) {
+  return ppc_impl_recv_ex(c, d, buf, bytes, mb, s, nullptr);
+}
+
+// pub != nullptr: the receive kernel also publishes that (prepared) zero-copy send once
+// this receive has completed (step driver fusion, ppc_step.cu)
+ppc_status_t ppc_impl_recv_ex(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t bytes,
+                              long long mb, cudaStream_t s, const PublishArgs* pub) {
   ppc_status_t st = check_live(c);
   if (st) return st;
   if (d != PPC_FWD && d != PPC_BWD) return PPC_ERR_INVALID_ARG;
@@ -558,6 +611,11 @@ ppc_status_t ppc_pp_recv(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t bytes, lo
   a.rec_dst = c->rank;
   a.seg_tab = c->seg_tab
       ? c->seg_tab + ((size_t)(d == PPC_FWD ? 0 : 1) * c->cfg.tp + c->tp_i) * kMaxSeg : nullptr;
+  if (pub) {
+    if (c->local_mode) return PPC_ERR_STATE;
+    a.has_pub = 1;
+    a.pub = *pub;
+  }
   if (c->capturing) {             // graph: relative seq, slot resolved on device
     a.sr = {c->dseq + 2 + d, (uint64_t)c->lay.stride, (uint32_t)c->K,
             std::max<uint32_t>(c->lay.max_chunks, 1), 0, 0};

@@ -133,7 +133,8 @@ struct ppc_comm {
   std::vector<int> members[3];
   cudaStream_t side[2] = {nullptr, nullptr};   // send streams of the step driver
   cudaStream_t zcw[2] = {nullptr, nullptr};    // step driver: zero-copy consumption waits
-  bool zc_side = true;                         // step driver publishes zero-copy on side[d]
+  bool zc_side = false;                        // step driver publishes zero-copy on side[d]
+  bool fuse_publish = true;                    // step driver: publish from the prior receive
   cudaStream_t ce[8] = {};                     // CE engine channel streams
   cudaEvent_t ce_fork = nullptr, ce_join[8] = {};
   ppc_record_t* trace_dev = nullptr;
@@ -162,11 +163,29 @@ struct ppc_comm {
   Blob blob{};
 };
 
+// A zero-copy send split in two (step driver fusion): the prepared publication, then the
+// rendezvous wait for its consumption.
+struct ZcSend {
+  PublishArgs p;
+  uint64_t target;          // credit to wait for (relative to *base when capturing)
+  const uint64_t* base;
+  ppc_dir_t d;
+};
+
 // internal entry points shared by the host translation units (not in the C ABI header)
 extern "C" {
 ppc_status_t ppc_impl_send_ex(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_t bytes,
                               long long mb, cudaStream_t s, cudaStream_t s_wait);
 int ppc_impl_is_zero_copy(const ppc_comm_t* c, const void* buf, size_t bytes);
+// bookkeeping + publication arguments of a zero-copy send, without launching anything
+ppc_status_t ppc_impl_zc_prepare(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_t bytes,
+                                 long long mb, ZcSend* z);
+// rendezvous wait of a published zero-copy send on s_wait (after the work queued on s)
+ppc_status_t ppc_impl_zc_commit(ppc_comm_t* c, const ZcSend& z, cudaStream_t s,
+                                cudaStream_t s_wait);
+// ppc_pp_recv whose kernel also publishes `pub` after completing (nullptr: plain receive)
+ppc_status_t ppc_impl_recv_ex(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t bytes,
+                              long long mb, cudaStream_t s, const PublishArgs* pub);
 }
 
 namespace ppc_impl {

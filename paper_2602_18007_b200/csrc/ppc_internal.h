@@ -68,6 +68,22 @@ struct PushArgs {
   uint32_t* done;               // completion counter (trace only)
 };
 
+// Zero-copy publication of a registered send buffer: credit wait, header, header flag.
+struct PublishArgs {
+  SeqRef sr;
+  SlotHeader* hdr;
+  uint64_t* hdr_flag;
+  const uint64_t* credit;
+  uint64_t need_credit;
+  uint64_t bytes, seq, src_off;
+  int64_t mb;
+  uint32_t src_seg, dir, boundary;
+  ErrWord* err;
+  uint64_t timeout_ns;
+  ppc_record_t* rec;              // trace: publish kernel entry .. header flag stored
+  int rec_src, rec_dst;
+};
+
 struct RecvArgs {
   SeqRef sr;
   uint8_t* dst;                 // user buffer
@@ -86,7 +102,12 @@ struct RecvArgs {
   ppc_record_t* rec;
   int rec_src, rec_dst;
   const uint64_t* seg_tab;      // zero-copy: mapped bases of the sender's registered buffers
+  // fused publication (step driver): when has_pub, the last CTA publishes `pub` (the next
+  // op's zero-copy send) right after releasing this receive's credit
+  uint32_t has_pub;
+  PublishArgs pub;
 };
+cudaError_t launch_publish(const PublishArgs& a, cudaStream_t s);
 
 // TP-sliced receive with a fused all-gather (ppc_pp_recv_gather).
 constexpr int kMaxTp = 8;
@@ -107,22 +128,6 @@ struct GatherArgs {
 };
 cudaError_t launch_gather(const GatherArgs& a, int grid, cudaStream_t s);
 
-// Zero-copy publication of a registered send buffer: credit wait, header, header flag.
-struct PublishArgs {
-  SeqRef sr;
-  SlotHeader* hdr;
-  uint64_t* hdr_flag;
-  const uint64_t* credit;
-  uint64_t need_credit;
-  uint64_t bytes, seq, src_off;
-  int64_t mb;
-  uint32_t src_seg, dir, boundary;
-  ErrWord* err;
-  uint64_t timeout_ns;
-  ppc_record_t* rec;              // trace: publish kernel entry .. header flag stored
-  int rec_src, rec_dst;
-};
-cudaError_t launch_publish(const PublishArgs& a, cudaStream_t s);
 
 // CE engine pieces: header/credit kernel before the copies, flag kernel after each.
 struct CeHeadArgs {

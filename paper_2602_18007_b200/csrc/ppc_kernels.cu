@@ -392,6 +392,34 @@ __global__ void __launch_bounds__(kWsThreads) push_ws_kernel(PushArgs a0) {
   }
 }
 
+// zero-copy publication (publish_kernel; fused into recv_kernel by the step driver)
+__device__ __forceinline__ void publish_body(const PublishArgs& a) {
+  const uint64_t t0 = globaltimer();
+  if (a.need_credit && !wait_geq(a.credit, a.need_credit, t0 + a.timeout_ns)) {
+    latch(a.err, PPC_ERR_TIMEOUT, a.seq, a.dir);
+    return;
+  }
+  SlotHeader h = {};
+  h.magic = kMagic;
+  h.dir = (uint8_t)a.dir;
+  h.boundary = (uint8_t)a.boundary;
+  h.flags = kHdrZeroCopy;
+  h.bytes = a.bytes;
+  h.seq = a.seq;
+  h.mb = a.mb;
+  h.src_off = a.src_off;
+  h.src_seg = a.src_seg;
+  const uint4* hs = reinterpret_cast<const uint4*>(&h);
+  uint4* hd = reinterpret_cast<uint4*>(a.hdr);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) st_data(hd + j, hs[j]);
+  st_release_sys(a.hdr_flag, a.seq);   // cumulative: the producer's writes to the buffer too
+  if (a.rec) {
+    fill_record(a.rec, (long long)t0, a.rec_src, a.rec_dst, (int)a.dir, 0, a.seq, a.mb, a.bytes);
+    a.rec->t_end_ns = (long long)globaltimer();
+  }
+}
+
 // ---------------------------------------------------------------- K10: recv + copy-out
 template <bool kSys>
 __global__ void __launch_bounds__(kThreads) recv_kernel(RecvArgs a0) {
@@ -456,6 +484,7 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(RecvArgs a0) {
       __threadfence();
       st_rel<kSys>(a.peer_credit, a.seq);
       if (a.rec) a.rec->t_end_ns = (long long)globaltimer();
+      if (a.has_pub) publish_body(resolve(a.pub));   // the next op's zero-copy send
     }
   }
 }
@@ -528,31 +557,7 @@ cudaError_t launch_gather(const GatherArgs& a, int grid, cudaStream_t s) {
 // waits for the receiver's credit (launch_wait_credit) before the buffer may be reused.
 __global__ void publish_kernel(PublishArgs a0) {
   pdl_enter();
-  const PublishArgs a = resolve(a0);
-  const uint64_t t0 = globaltimer();
-  if (a.need_credit && !wait_geq(a.credit, a.need_credit, t0 + a.timeout_ns)) {
-    latch(a.err, PPC_ERR_TIMEOUT, a.seq, a.dir);
-    return;
-  }
-  SlotHeader h = {};
-  h.magic = kMagic;
-  h.dir = (uint8_t)a.dir;
-  h.boundary = (uint8_t)a.boundary;
-  h.flags = kHdrZeroCopy;
-  h.bytes = a.bytes;
-  h.seq = a.seq;
-  h.mb = a.mb;
-  h.src_off = a.src_off;
-  h.src_seg = a.src_seg;
-  const uint4* hs = reinterpret_cast<const uint4*>(&h);
-  uint4* hd = reinterpret_cast<uint4*>(a.hdr);
-#pragma unroll
-  for (int j = 0; j < 4; ++j) st_data(hd + j, hs[j]);
-  st_release_sys(a.hdr_flag, a.seq);   // cumulative: the producer's writes to the buffer too
-  if (a.rec) {
-    fill_record(a.rec, (long long)t0, a.rec_src, a.rec_dst, (int)a.dir, 0, a.seq, a.mb, a.bytes);
-    a.rec->t_end_ns = (long long)globaltimer();
-  }
+  publish_body(resolve(a0));
 }
 
 cudaError_t launch_publish(const PublishArgs& a, cudaStream_t s) {

@@ -91,6 +91,7 @@ struct Stepper {
   // direct mode: inbox[d] = messages sent to this stage in direction d; out[d] = receiver's
   Mailbox* inbox[2] = {nullptr, nullptr};
   Mailbox* outbox[2] = {nullptr, nullptr};
+  bool fused_next = false;      // the next op's send was fused into this op's receive
   bool dmode = false;
   cudaStream_t xq = nullptr;    // direct mode: the GPU's transfer queue (nullptr: own stream)
 
@@ -110,6 +111,26 @@ struct Stepper {
   }
 
   bool done() const { return i == ops.size(); }
+
+  // Fusion of "terminal receive, then a zero-copy send with no stage compute in between"
+  // (both ends of a comm-only PP2 step: F_m lands in y[m], then B_m leaves from g[m]).
+  // The next op is a source op (no input, no stage function) whose registered source is
+  // published from the compute stream: its publication then rides on this receive's
+  // kernel (the last CTA writes the header right after the credit), saving one kernel
+  // boundary on the critical path.  The order of the two ops is unchanged.
+  // PPC_FUSE_PUBLISH=0 disables it.
+  bool fusable_next(ZcSend* z) {
+    if (i + 1 >= ops.size() || c->zc_side || !c->fuse_publish) return false;
+    const int kind = ops[i + 1].kind, m = ops[i + 1].mb;
+    const bool has_in = kind == 0 ? s > 0 : s < S - 1;
+    const bool has_out = kind == 0 ? s < S - 1 : s > 0;
+    if (has_in || !has_out || (kind == 0 ? st->fwd : st->bwd)) return false;
+    const void* const* srcs = kind == 0 ? st->x : st->g;
+    const void* src = srcs ? srcs[m] : nullptr;
+    const size_t bytes = kind == 0 ? st->fwd_bytes : st->bwd_bytes;
+    if (!src || !bytes || is_host_ptr(src) || !ppc_impl_is_zero_copy(c, src, bytes)) return false;
+    return ppc_impl_zc_prepare(c, (ppc_dir_t)kind, src, bytes, m, z) == PPC_OK;
+  }
 
   // direct mode: may the stage overwrite its buffer (kind 1 = rbuf, 2 = obuf) [d][bi]?
   // false = the receiving stage has not enqueued its copy yet (caller returns, retries).
@@ -151,10 +172,8 @@ struct Stepper {
             if (p.bytes != bytes) return PPC_ERR_SIZE_MISMATCH;
             if (p.mb != m) return PPC_ERR_ORDER;
             box.pop_front();
-            // the copy runs on the GPU's single transfer queue (xq) when there is one:
-            // copies are HBM-bound, so running two at once only splits the bandwidth;
-            // one at a time each gets all of it and the queue order (the round-robin
-            // enqueue order) already respects every dependency
+            // with PPC_LOCAL_QUEUE the copy runs on the GPU's single transfer queue (xq);
+            // the queue order (the round-robin enqueue order) respects every dependency
             cudaStream_t q = xq ? xq : cs;
             if (xq) {
               CK(cudaEventRecord(sb.xgo, cs));
@@ -177,10 +196,19 @@ struct Stepper {
             }
           } else {
             if (!dst && sb.rpending[d][bi]) CK(cudaStreamWaitEvent(cs, sb.rfree[d][bi], 0));
-            ppc_status_t rs = ppc_pp_recv(c, (ppc_dir_t)d, r, bytes, m, cs);
+            ZcSend z;
+            const bool fuse = dst && fusable_next(&z);
+            ppc_status_t rs = ppc_impl_recv_ex(c, (ppc_dir_t)d, r, bytes, m, cs,
+                                               fuse ? &z.p : nullptr);
             if (rs == PPC_ERR_WOULD_BLOCK) return PPC_OK;
             if (rs) return rs;
             if (!dst) sb.rpending[d][bi] = false;
+            if (fuse) {   // the next op's send was published by this receive's kernel
+              if (ppc_status_t ts = time_mark(c, 0, cs, true)) return ts;
+              if (ppc_status_t ws = ppc_impl_zc_commit(c, z, cs, c->side[z.d])) return ws;
+              if (ppc_status_t ts = time_mark(c, 0, c->side[z.d], false)) return ts;
+              fused_next = true;
+            }
           }
           direct = dst != nullptr;
           in = r;
@@ -265,7 +293,9 @@ struct Stepper {
         phase = 2;
       }
       if (phase == 2) {                                  // send
-        if (has_out) {
+        if (has_out && fused_next) {
+          fused_next = false;                            // already published (fusion)
+        } else if (has_out) {
           if (dmode) {
             // hand the buffer to the next stage: it makes the one copy
             cudaEvent_t rdy = sb.dready[d][bi];
@@ -360,7 +390,11 @@ extern "C" ppc_status_t ppc_step_1f1b_local(ppc_comm_t* const* comms, int S,
   std::vector<Mailbox> box(2 * S);
   const bool dmode = S > 1 && same_device && env_int("PPC_LOCAL_DIRECT", 1) != 0;
   cudaStream_t xq = nullptr;
-  if (dmode && env_int("PPC_LOCAL_QUEUE", 1) != 0) {
+  // PPC_LOCAL_QUEUE=1: all copies of the GPU on one transfer queue.  Measured slower than
+  // letting each stage copy on its own stream (C2: 219 vs 188 us per step,
+  // profiles/r34_n1_queue.jsonl): one 32 MiB copy alone does not saturate HBM, two
+  // concurrent ones do.  Kept as an option; off by default.
+  if (dmode && env_int("PPC_LOCAL_QUEUE", 0) != 0) {
     ppc_comm* c0 = comms[0];
     DeviceGuard g(c0->device);
     if (!c0->sb.xq) {
