@@ -63,8 +63,17 @@ bool alloc_range(const void* p, uintptr_t* base, size_t* size) {
   return true;
 }
 
+// Zero-copy source lookup: index of the registered segment holding [p, p+bytes), or
+// kArenaSeg for the step driver's buffers in our own arena (PPC_ZC_STEPBUFS), else -1.
 int find_reg(const ppc_comm* c, const void* p, size_t bytes, uint64_t* off) {
   const uintptr_t a = (uintptr_t)p;
+  if (c->arena && c->zc_stepbufs) {
+    const uintptr_t s0 = (uintptr_t)c->arena + c->lay.step;
+    if (a >= s0 && a + bytes <= s0 + 8 * c->lay.stride) {
+      *off = a - (uintptr_t)c->arena;
+      return (int)kArenaSeg;
+    }
+  }
   for (size_t i = 0; i < c->regs.size(); ++i) {
     const auto& r = c->regs[i];
     if (a >= r.base && a + bytes <= r.base + r.size) {
@@ -141,6 +150,7 @@ ppc_status_t ppc_create(const ppc_config_t* cfg, int world, int rank, int cuda_d
   if (c->cfg.channels == 0) c->cfg.channels = 1;
   c->zc_side = env_int("PPC_ZC_SIDE", 0) != 0;
   c->fuse_publish = env_int("PPC_FUSE_PUBLISH", 1) != 0;
+  c->zc_stepbufs = env_int("PPC_ZC_STEPBUFS", 1) != 0;
   ppc::g_pdl = env_int("PPC_PDL", 1) != 0 ? 1 : 0;
   const int tp = cfg->tp, dp = cfg->dp;
   c->pp_i = rank / (tp * dp);
@@ -328,6 +338,7 @@ ppc_status_t ppc_connect(ppc_comm_t* c, const void* all_blobs, size_t blob_bytes
         h.i_flags = (uint64_t*)(c->arena + L.flags[d]);
         h.i_done = (uint32_t*)(c->arena + L.done[d]);
         h.peer_credit = (uint64_t*)(ib + L.credit[d]);
+        h.i_arena = ib;
         if (c->local_mode) h.in_comm = (ppc_comm*)(uintptr_t)B[h.peer_in].comm_ptr;
       }
       if (c->local_mode) {
@@ -368,7 +379,7 @@ ppc_status_t ppc_group(const ppc_comm_t* c, ppc_group_t g, int* members, int* n,
 
 int ppc_impl_is_zero_copy(const ppc_comm_t* c, const void* buf, size_t bytes) {
   uint64_t off = 0;
-  return c && !c->local_mode && bytes > 0 && buf && find_reg(c, buf, bytes, &off) >= 0;
+  return c && !c->local_mode && bytes > 0 && buf && find_reg(c, buf, bytes, &off) != -1;
 }
 
 }  // extern "C"
@@ -437,7 +448,7 @@ ppc_status_t ppc_impl_zc_prepare(ppc_comm_t* c, ppc_dir_t d, const void* buf, si
   if (c->device < 0 || c->local_mode) return PPC_ERR_STATE;
   uint64_t zc_off = 0;
   const int zc_seg = find_reg(c, buf, bytes, &zc_off);
-  if (zc_seg < 0) return PPC_ERR_INVALID_ARG;
+  if (zc_seg == -1) return PPC_ERR_INVALID_ARG;
   const uint64_t seq = h.send_seq + 1;
   const uint64_t need = seq > (uint64_t)c->K ? seq - c->K : 0;
   fill_publish(c, d, seq, need, bytes, mb, zc_seg, zc_off, next_record(c), z);
@@ -485,7 +496,7 @@ ppc_status_t ppc_impl_send_ex(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_
   if (ppc_status_t ts = time_mark(c, 0, s, true)) return ts;
   uint64_t zc_off = 0;
   const int zc_seg = (!c->local_mode && bytes > 0) ? find_reg(c, buf, bytes, &zc_off) : -1;
-  if (zc_seg >= 0) {              // registered buffer: publish it, the receiver pulls it
+  if (zc_seg != -1) {              // registered buffer: publish it, the receiver pulls it
     ZcSend z;
     fill_publish(c, d, seq, need, bytes, mb, zc_seg, zc_off, rec, &z);
     CK(launch_publish(z.p, s));
@@ -611,6 +622,7 @@ ppc_status_t ppc_impl_recv_ex(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t byte
   a.rec_dst = c->rank;
   a.seg_tab = c->seg_tab
       ? c->seg_tab + ((size_t)(d == PPC_FWD ? 0 : 1) * c->cfg.tp + c->tp_i) * kMaxSeg : nullptr;
+  a.peer_arena = h.i_arena;
   if (pub) {
     if (c->local_mode) return PPC_ERR_STATE;
     a.has_pub = 1;
@@ -917,8 +929,8 @@ ppc_status_t ppc_destroy(ppc_comm_t* c) {
     StepBufs& sb = c->sb;
     for (int d = 0; d < 2; ++d)
       for (int i = 0; i < 2; ++i) {
-        if (sb.rbuf[d][i]) cudaFree(sb.rbuf[d][i]);
-        if (sb.obuf[d][i]) cudaFree(sb.obuf[d][i]);
+        if (sb.rbuf[d][i] && !sb.in_arena) cudaFree(sb.rbuf[d][i]);
+        if (sb.obuf[d][i] && !sb.in_arena) cudaFree(sb.obuf[d][i]);
         if (sb.hbuf[d][i]) cudaFree(sb.hbuf[d][i]);
         if (sb.rfree[d][i]) cudaEventDestroy(sb.rfree[d][i]);
         if (sb.ofree[d][i]) cudaEventDestroy(sb.ofree[d][i]);

@@ -45,6 +45,7 @@ struct Layout {
   size_t stride = 0;             // slot payload stride
   size_t payload[2] = {}, hdr[2] = {}, hdr_flag[2] = {}, flags[2] = {}, credit[2] = {},
          done[2] = {}, push_done[2] = {}, gdone[2] = {};
+  size_t step = 0;               // step driver buffers: [recv|out][dir][2] x stride
   size_t total = 0;
   uint32_t max_chunks = 0;
   void build(int K, size_t max_msg, size_t chunk) {
@@ -52,6 +53,10 @@ struct Layout {
     max_chunks = (uint32_t)((max_msg + chunk - 1) / chunk);
     size_t off = 0;
     for (int d = 0; d < 2; ++d) { payload[d] = off; off += (size_t)K * stride; }
+    // the step driver's receive / output buffers, so a middle stage can forward a message
+    // zero-copy (the next stage pulls it from this arena, already mapped there)
+    step = off;
+    off += 8 * stride;
     for (int d = 0; d < 2; ++d) { hdr[d] = off; off = round_up(off + (size_t)K * 64, 256); }
     for (int d = 0; d < 2; ++d) { hdr_flag[d] = off; off = round_up(off + (size_t)K * 8, 256); }
     for (int d = 0; d < 2; ++d) {
@@ -86,6 +91,7 @@ struct Chan {
   uint64_t* i_flags = nullptr;
   uint32_t* i_done = nullptr;
   uint64_t* peer_credit = nullptr;   // in the sender's arena
+  const uint8_t* i_arena = nullptr;  // the sender's arena (zero-copy from its step buffers)
   uint64_t recv_seq = 0;
   ppc_comm* in_comm = nullptr;
   // virtual-stage mode: stream ordering through events
@@ -97,6 +103,7 @@ struct StepBufs {
   uint8_t* rbuf[2][2] = {};     // [dir][i] recv landing
   uint8_t* obuf[2][2] = {};     // [dir][i] stage output
   uint8_t* hbuf[2][2] = {};     // [dir][i] staging for host inputs / outputs
+  bool in_arena = false;        // rbuf / obuf are the arena's step region (not freed here)
   cudaEvent_t rfree[2][2] = {}, ofree[2][2] = {}, ready = nullptr, join[2] = {};
   bool rpending[2][2] = {}, opending[2][2] = {};
   // direct (single-copy) mode of same-GPU virtual stages: [dir][i] of the buffer handed to
@@ -135,6 +142,7 @@ struct ppc_comm {
   cudaStream_t zcw[2] = {nullptr, nullptr};    // step driver: zero-copy consumption waits
   bool zc_side = false;                        // step driver publishes zero-copy on side[d]
   bool fuse_publish = true;                    // step driver: publish from the prior receive
+  bool zc_stepbufs = true;                     // step driver buffers are zero-copy sources
   cudaStream_t ce[8] = {};                     // CE engine channel streams
   cudaEvent_t ce_fork = nullptr, ce_join[8] = {};
   ppc_record_t* trace_dev = nullptr;

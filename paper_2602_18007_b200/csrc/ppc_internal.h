@@ -11,6 +11,8 @@ constexpr int kThreads = 512;                // CTA size of the copy kernels
 constexpr int kMaxSlots = 64;
 constexpr int kMaxSeg = 256;                 // registered send buffers per peer
 constexpr uint16_t kHdrZeroCopy = 1;         // header flag: payload is in a registered buffer
+constexpr uint32_t kArenaSeg = 0xFFFFFFFFu;  // zero-copy src_seg: the sender's own arena
+                                             // (the step driver's buffers live there)
 
 // 64-byte slot header, little-endian.  Ring path: the payload is in
 // the slot.  Zero-copy path (flags & kHdrZeroCopy): the payload stays in the sender's
@@ -102,6 +104,7 @@ struct RecvArgs {
   ppc_record_t* rec;
   int rec_src, rec_dst;
   const uint64_t* seg_tab;      // zero-copy: mapped bases of the sender's registered buffers
+  const uint8_t* peer_arena;    // zero-copy from the sender's arena (src_seg == kArenaSeg)
   // fused publication (step driver): when has_pub, the last CTA publishes `pub` (the next
   // op's zero-copy send) right after releasing this receive's credit
   uint32_t has_pub;

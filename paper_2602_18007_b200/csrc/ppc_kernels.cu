@@ -447,7 +447,8 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(RecvArgs a0) {
         fail = 1;
       } else if (h->flags & kHdrZeroCopy) {
         const uint32_t seg = h->src_seg;
-        const uint64_t base = (a.seg_tab && seg < (uint32_t)kMaxSeg) ? a.seg_tab[seg] : 0;
+        const uint64_t base = seg == kArenaSeg ? (uint64_t)(uintptr_t)a.peer_arena
+                            : (a.seg_tab && seg < (uint32_t)kMaxSeg) ? a.seg_tab[seg] : 0;
         if (!base) {                   // the receiver never imported that registration
           latch(a.err, PPC_ERR_ORDER, a.seq, 0x300u | seg << 12);
           fail = 1;

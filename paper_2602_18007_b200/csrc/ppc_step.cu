@@ -43,17 +43,28 @@ ppc_status_t ensure_bufs(ppc_comm* c, size_t bytes) {
   }
   if (bytes <= sb.bytes) return PPC_OK;
   CK(cudaDeviceSynchronize());
+  // messages up to max_msg_bytes: the arena's step region (zeroed at create; a peer can
+  // pull a forwarded message from it, zero-copy); larger scratch falls back to cudaMalloc
+  const bool arena = c->arena && bytes <= c->lay.stride;
   for (int d = 0; d < 2; ++d)
     for (int i = 0; i < 2; ++i) {
-      if (sb.rbuf[d][i]) cudaFree(sb.rbuf[d][i]);
-      if (sb.obuf[d][i]) cudaFree(sb.obuf[d][i]);
+      if (!sb.in_arena) {
+        if (sb.rbuf[d][i]) cudaFree(sb.rbuf[d][i]);
+        if (sb.obuf[d][i]) cudaFree(sb.obuf[d][i]);
+      }
       sb.rbuf[d][i] = sb.obuf[d][i] = nullptr;
-      CK(cudaMalloc(&sb.rbuf[d][i], bytes));
-      CK(cudaMalloc(&sb.obuf[d][i], bytes));
-      CK(cudaMemset(sb.obuf[d][i], 0, bytes));
+      if (arena) {
+        sb.rbuf[d][i] = c->arena + c->lay.step + (size_t)((0 * 2 + d) * 2 + i) * c->lay.stride;
+        sb.obuf[d][i] = c->arena + c->lay.step + (size_t)((1 * 2 + d) * 2 + i) * c->lay.stride;
+      } else {
+        CK(cudaMalloc(&sb.rbuf[d][i], bytes));
+        CK(cudaMalloc(&sb.obuf[d][i], bytes));
+        CK(cudaMemset(sb.obuf[d][i], 0, bytes));
+      }
       sb.rpending[d][i] = sb.opending[d][i] = false;
     }
-  sb.bytes = bytes;
+  sb.in_arena = arena;
+  sb.bytes = arena ? c->lay.stride : bytes;
   return PPC_OK;
 }
 

@@ -406,6 +406,12 @@ def main():
         comm = case_hetero(rank, world)
     elif case == "zc":
         comm = case_zc(rank, world)
+    elif case == "zc_unfused":           # publication by its own kernel (PPC_FUSE_PUBLISH=0)
+        os.environ["PPC_FUSE_PUBLISH"] = "0"
+        comm = case_zc(rank, world)
+    elif case == "zc_side":              # publication on the send stream (PPC_ZC_SIDE=1)
+        os.environ["PPC_ZC_SIDE"] = "1"
+        comm = case_zc(rank, world)
     elif case == "graph":
         comm = case_graph(rank, world)
     elif case == "fullsize":

@@ -45,8 +45,12 @@ def test_hetero_allreduce(n):
     _run("hetero", n)
 
 
-def test_zero_copy_registered_pull():
-    _run("zc", 2)
+@pytest.mark.parametrize("case", ["zc", "zc_unfused", "zc_side"])
+def test_zero_copy_registered_pull(case):
+    """Default: the step driver fuses each source op's publication into the preceding
+    terminal receive kernel; the other two cases cover the unfused publication kernel on
+    the compute stream and on the send stream."""
+    _run(case, 2)
 
 
 @pytest.mark.parametrize("n", [2, 4])
