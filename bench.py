@@ -50,10 +50,12 @@ def parse():
     ap.add_argument("--graph", type=int, default=1,
                     help="replay the step as one CUDA graph (ppc_graph_create)")
     ap.add_argument("--zc", type=int, default=-1,
-                    help="N>=2: register the step's send buffers (zero-copy NVLink pulls); "
+                    help="N>=2: register the step's source buffers (zero-copy NVLink pulls); "
                          "-1 = on for pp = 2 (every send is then a pull), off for deeper "
-                         "pipelines (middle stages forward from unregistered buffers and "
-                         "mixing pulls with pushes on one link measured slower)")
+                         "pipelines: a pull moves data only when the receiver reaches its "
+                         "receive, while a push runs ahead into the K-slot ring, which the "
+                         "warm-up of a deep 1F1B pipeline exploits (PP4 M16: 3623 us "
+                         "all-pull vs 2868 us, profiles/r38_pp4_zc_vs_ring.jsonl)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -378,6 +380,13 @@ def main():
                                "note": "this process's transfer launches of the step (both "
                                        "directions, concurrent) over the instrumented step time"},
             "recv_avg_launch_us": (statistics.mean(recv_ms) * 1e3) if recv_ms else None}
+    # launches of the dominant kernel overlap (the F and B transfers of a 1F1B step run
+    # concurrently and share the bandwidth), so per-launch "achieved" is ~1/concurrency of
+    # what the kernel class moves; report the measured overlap beside it
+    if push_ms and ms_instr > 0:
+        conc = sum(push_ms) / (len(comms) * ms_instr)
+        roof["concurrency"] = conc
+        roof["frac_x_concurrency"] = roof["frac"] * conc
     if distributed and args.zc and recv_recs:
         phase_us = statistics.mean((r["t_end_ns"] - r["t_start_ns"]) * 1e-3 for r in recv_recs)
         phase_us = max_over_ranks(phase_us)

@@ -939,6 +939,14 @@ ppc_status_t ppc_destroy(ppc_comm_t* c) {
     if (sb.xgo) cudaEventDestroy(sb.xgo);
     if (sb.xdone) cudaEventDestroy(sb.xdone);
     if (sb.xq) cudaStreamDestroy(sb.xq);
+    if (sb.ds) cudaStreamDestroy(sb.ds);
+    if (sb.dgo) cudaEventDestroy(sb.dgo);
+    if (sb.djoin) cudaEventDestroy(sb.djoin);
+    for (int d = 0; d < 2; ++d)
+      for (int i = 0; i < 2; ++i) {
+        if (sb.dfree_r[d][i]) cudaEventDestroy(sb.dfree_r[d][i]);
+        if (sb.dfree_o[d][i]) cudaEventDestroy(sb.dfree_o[d][i]);
+      }
     for (int d = 0; d < 2; ++d) if (sb.join[d]) cudaEventDestroy(sb.join[d]);
     for (int d = 0; d < 2; ++d) {
       if (c->side[d]) cudaStreamDestroy(c->side[d]);

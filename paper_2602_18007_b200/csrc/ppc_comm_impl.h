@@ -104,6 +104,11 @@ struct StepBufs {
   uint8_t* obuf[2][2] = {};     // [dir][i] stage output
   uint8_t* hbuf[2][2] = {};     // [dir][i] staging for host inputs / outputs
   bool in_arena = false;        // rbuf / obuf are the arena's step region (not freed here)
+  // device->host copies of terminal outputs run on ds (overlapping the next op's host->device
+  // copy and transfers); dfree_[ro] = that copy finished reading rbuf / obuf [dir][i]
+  cudaStream_t ds = nullptr;
+  cudaEvent_t dgo = nullptr, djoin = nullptr, dfree_r[2][2] = {}, dfree_o[2][2] = {};
+  bool dpend_r[2][2] = {}, dpend_o[2][2] = {};
   cudaEvent_t rfree[2][2] = {}, ofree[2][2] = {}, ready = nullptr, join[2] = {};
   bool rpending[2][2] = {}, opending[2][2] = {};
   // direct (single-copy) mode of same-GPU virtual stages: [dir][i] of the buffer handed to

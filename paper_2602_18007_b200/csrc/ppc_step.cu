@@ -30,6 +30,9 @@ ppc_status_t ensure_bufs(ppc_comm* c, size_t bytes) {
     CK(cudaEventCreateWithFlags(&sb.ready, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&sb.xgo, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&sb.xdone, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&sb.dgo, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&sb.djoin, cudaEventDisableTiming));
+    CK(cudaStreamCreateWithFlags(&sb.ds, cudaStreamNonBlocking));
     for (int d = 0; d < 2; ++d) {
       CK(cudaEventCreateWithFlags(&sb.join[d], cudaEventDisableTiming));
       for (int i = 0; i < 2; ++i) {
@@ -38,6 +41,8 @@ ppc_status_t ensure_bufs(ppc_comm* c, size_t bytes) {
         CK(cudaEventCreateWithFlags(&sb.dready[d][i], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&sb.cons_r[d][i], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&sb.cons_o[d][i], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&sb.dfree_r[d][i], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&sb.dfree_o[d][i], cudaEventDisableTiming));
       }
     }
   }
@@ -103,6 +108,7 @@ struct Stepper {
   Mailbox* inbox[2] = {nullptr, nullptr};
   Mailbox* outbox[2] = {nullptr, nullptr};
   bool fused_next = false;      // the next op's send was fused into this op's receive
+  bool used_ds = false;         // a terminal output went to host memory through sb.ds
   bool dmode = false;
   cudaStream_t xq = nullptr;    // direct mode: the GPU's transfer queue (nullptr: own stream)
 
@@ -122,6 +128,35 @@ struct Stepper {
   }
 
   bool done() const { return i == ops.size(); }
+
+  // before `st` writes rbuf / obuf [d][bi]: wait for a pending device->host read of it
+  ppc_status_t before_write(int kind, int d, int bi, cudaStream_t q) {
+    StepBufs& sb = c->sb;
+    bool* pend = kind == 1 ? &sb.dpend_r[d][bi] : &sb.dpend_o[d][bi];
+    if (*pend) {
+      CK(cudaStreamWaitEvent(q, kind == 1 ? sb.dfree_r[d][bi] : sb.dfree_o[d][bi], 0));
+      *pend = false;
+    }
+    return PPC_OK;
+  }
+
+  // terminal output to host memory: copy on the D2H stream (kind: 1 = src is rbuf [d][bi],
+  // 2 = obuf [d][bi], 0 = a caller buffer)
+  ppc_status_t d2h(void* dst, const void* src, size_t bytes, int kind, int d, int bi) {
+    StepBufs& sb = c->sb;
+    CK(cudaEventRecord(sb.dgo, cs));
+    CK(cudaStreamWaitEvent(sb.ds, sb.dgo, 0));
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, sb.ds));
+    if (kind == 1) {
+      CK(cudaEventRecord(sb.dfree_r[d][bi], sb.ds));
+      sb.dpend_r[d][bi] = true;
+    } else if (kind == 2) {
+      CK(cudaEventRecord(sb.dfree_o[d][bi], sb.ds));
+      sb.dpend_o[d][bi] = true;
+    }
+    used_ds = true;
+    return PPC_OK;
+  }
 
   // Fusion of "terminal receive, then a zero-copy send with no stage compute in between"
   // (both ends of a comm-only PP2 step: F_m lands in y[m], then B_m leaves from g[m]).
@@ -186,6 +221,8 @@ struct Stepper {
             // with PPC_LOCAL_QUEUE the copy runs on the GPU's single transfer queue (xq);
             // the queue order (the round-robin enqueue order) respects every dependency
             cudaStream_t q = xq ? xq : cs;
+            if (!dst)
+              if (ppc_status_t w = before_write(1, d, bi, cs)) return w;
             if (xq) {
               CK(cudaEventRecord(sb.xgo, cs));
               CK(cudaStreamWaitEvent(xq, sb.xgo, 0));
@@ -207,6 +244,8 @@ struct Stepper {
             }
           } else {
             if (!dst && sb.rpending[d][bi]) CK(cudaStreamWaitEvent(cs, sb.rfree[d][bi], 0));
+            if (!dst)
+              if (ppc_status_t w = before_write(1, d, bi, cs)) return w;
             ZcSend z;
             const bool fuse = dst && fusable_next(&z);
             ppc_status_t rs = ppc_impl_recv_ex(c, (ppc_dir_t)d, r, bytes, m, cs,
@@ -235,6 +274,7 @@ struct Stepper {
               CK(cudaStreamWaitEvent(cs, sb.rfree[d][bi], 0));
             }
             sb.rpending[d][bi] = false;
+            if (ppc_status_t w = before_write(1, d, bi, cs)) return w;
             CK(cudaMemcpyAsync(r, in, bytes, cudaMemcpyHostToDevice, cs));
             in = r;
           }
@@ -254,6 +294,7 @@ struct Stepper {
               CK(cudaStreamWaitEvent(cs, sb.ofree[d][bi], 0));
             }
             uint8_t* o = sb.obuf[d][bi];
+            if (ppc_status_t w = before_write(2, d, bi, cs)) return w;
             if (fn && fn(user, m, in, o, in ? bytes : 0, bytes, cs) != 0) return PPC_ERR_INVALID_ARG;
             send_src = o;          // no input and no fn: scratch contents
             send_free = sb.ofree[d][bi];
@@ -294,10 +335,17 @@ struct Stepper {
             }
             uint8_t* o = sb.obuf[d][bi];
             void* target = (dst && !host) ? dst : o;
+            if (target == o)
+              if (ppc_status_t w = before_write(2, d, bi, cs)) return w;
             if (fn(user, m, in, target, in ? bytes : 0, bytes, cs) != 0) return PPC_ERR_INVALID_ARG;
-            if (host) CK(cudaMemcpyAsync(dst, o, bytes, cudaMemcpyDeviceToHost, cs));
+            if (host)
+              if (ppc_status_t w = d2h(dst, o, bytes, 2, d, bi)) return w;
           } else if (dst && in && bytes && !direct) {
-            CK(cudaMemcpyAsync(dst, in, bytes, cudaMemcpyDefault, cs));
+            if (is_host_ptr(dst)) {
+              if (ppc_status_t w = d2h(dst, in, bytes, in == sb.rbuf[d][bi] ? 1 : 0, d, bi)) return w;
+            } else {
+              CK(cudaMemcpyAsync(dst, in, bytes, cudaMemcpyDefault, cs));
+            }
           }
         }
         *progressed = true;
@@ -347,6 +395,10 @@ struct Stepper {
   }
 
   ppc_status_t finish() {
+    if (used_ds) {                 // host outputs complete with the step
+      CK(cudaEventRecord(c->sb.djoin, c->sb.ds));
+      CK(cudaStreamWaitEvent(cs, c->sb.djoin, 0));
+    }
     if (dmode) return PPC_OK;
     for (int d = 0; d < 2; ++d) {
       // join only the send streams this stage used (an unused one is not part of a graph

@@ -181,6 +181,51 @@ def test_xor_1f1b_step_matches_oracle(S, M, engine, direct, monkeypatch):
 
 
 @pytest.mark.parametrize("direct", [1, 0])
+@pytest.mark.parametrize("fn", [True, False])
+@pytest.mark.parametrize("S", [2, 3])
+def test_step_with_host_buffers(S, fn, direct, monkeypatch):
+    """The e2e path: pinned HOST inputs X / G and outputs Y / DX.  Host inputs are staged
+    into the step buffers, terminal outputs leave on the device->host stream while the next
+    ops proceed; repeated steps exercise buffer reuse behind those copies.  fn=True: XOR
+    stage functions (outputs via the stage-output buffers); fn=False: identity."""
+    monkeypatch.setenv("PPC_LOCAL_DIRECT", str(direct))
+    M, n = 6, 2 * (64 << 10) + 777
+    cfg = ppc.make_config(pp=S, max_msg_bytes=n, chunk_bytes=64 << 10)
+    comms = ppc.virtual_stages(cfg, DEV)
+    hX = [torch.from_numpy(P.source_activation(42, 0, m, n).copy()).pin_memory() for m in range(M)]
+    hG = [torch.from_numpy(P.source_gradient(42, 0, m, n).copy()).pin_memory() for m in range(M)]
+    hY = [torch.zeros(n, dtype=torch.uint8).pin_memory() for _ in range(M)]
+    hDX = [torch.zeros(n, dtype=torch.uint8).pin_memory() for _ in range(M)]
+    ctx = [(ppc.XorCtx(42, 0, s, 0), ppc.XorCtx(42, 0, s, 1)) for s in range(S)]
+    args = [ppc.StepArgs(M, n, n, fwd=ppc.STAGE_XOR if fn else None,
+                         bwd=ppc.STAGE_XOR if fn else None,
+                         fwd_user=ctx[s][0] if fn else None, bwd_user=ctx[s][1] if fn else None,
+                         x=hX if s == 0 else None, g=hG if s == S - 1 else None,
+                         y=hY if s == S - 1 else None, dx=hDX if s == 0 else None)
+            for s in range(S)]
+    streams = [torch.cuda.Stream() for _ in range(S)]
+    mask = _masks(n)
+    ident = lambda s_, m, x: x
+    f = xor_stage(mask, 0) if fn else ident
+    b = xor_stage(mask, 1) if fn else ident
+    Yo, DXo, _, _ = run_1f1b(S, M, 2, f, b, lambda m: P.source_activation(42, 0, m, n),
+                             lambda m: P.source_gradient(42, 0, m, n), n, n, n)
+    for _ in range(3):
+        for t in hY + hDX:
+            t.zero_()
+        ppc.step_1f1b_local(comms, args, streams)
+        torch.cuda.synchronize()
+        for m in range(M):
+            assert np.array_equal(hY[m].numpy(), Yo[m]), m
+            assert np.array_equal(hDX[m].numpy(), DXo[m]), m
+    for c in comms:
+        assert c.poll() == 0
+        c.disconnect()
+    for c in comms:
+        c.destroy()
+
+
+@pytest.mark.parametrize("direct", [1, 0])
 @pytest.mark.parametrize("S", [2, 3])
 def test_xor_step_cuda_graph(S, direct, monkeypatch):
     """A step captured into a CUDA graph (relative sequence numbers on device) replays
