@@ -384,7 +384,7 @@ def main():
     # concurrently and share the bandwidth), so per-launch "achieved" is ~1/concurrency of
     # what the kernel class moves; report the measured overlap beside it
     if push_ms and ms_instr > 0:
-        conc = sum(push_ms) / (len(comms) * ms_instr)
+        conc = sum(push_ms) / ms_instr       # this process's launches (all its stages)
         roof["concurrency"] = conc
         roof["frac_x_concurrency"] = roof["frac"] * conc
     if distributed and args.zc and recv_recs:
