@@ -26,6 +26,19 @@
  *    ppc_destroy, then a fresh ppc_create.
  *  - Every device wait is bounded by cfg.timeout_ns (%globaltimer); no unbounded spin
  *    (§4.3: "training frequently encountered hang issues").
+ *
+ * Environment (read by ppc_create / the step driver; defaults are the measured best,
+ * DESIGN.md §6-7):
+ *   PPC_PDL=1            programmatic dependent launch of the transport kernels
+ *   PPC_FUSE_PUBLISH=1   step driver: a zero-copy source op's publication rides on the
+ *                        preceding terminal receive kernel
+ *   PPC_ZC_SIDE=0        step driver: publish zero-copy sends on the send stream instead
+ *                        of the compute stream
+ *   PPC_ZC_STEPBUFS=1    the step driver's buffers (in the arena) are zero-copy sources
+ *   PPC_LOCAL_DIRECT=1   virtual stages: single-copy hand-off instead of the ring
+ *   PPC_LOCAL_QUEUE=0    virtual stages: serialise all copies of the GPU on one queue
+ *   PPC_COPY_CTAS=296    virtual stages: CTAs of the hand-off copy kernel
+ *   PPC_RECV_CTAS, PPC_STAGE_CTAS, PPC_PUSH_WS=1   grid / kernel-variant overrides
  */
 #ifndef PPC_H_
 #define PPC_H_

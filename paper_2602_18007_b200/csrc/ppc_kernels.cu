@@ -63,6 +63,12 @@ __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
 __device__ __forceinline__ void fence_acq_rel_sys() {
   asm volatile("fence.acq_rel.sys;" ::: "memory");
 }
+__device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_gpu(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 // Scope-templated variants: kSys = peer GPU over NVLink (.sys); !kSys = virtual stages on
 // one GPU, where the consumer is on the same device (.gpu is enough and cheaper).
 __device__ __forceinline__ uint64_t ld_acquire_gpu(const uint64_t* p) {
@@ -80,6 +86,10 @@ __device__ __forceinline__ uint64_t ld_acq(const uint64_t* p) {
 template <bool kSys>
 __device__ __forceinline__ void st_rel(uint64_t* p, uint64_t v) {
   if (kSys) st_release_sys(p, v); else st_release_gpu(p, v);
+}
+template <bool kSys>
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
+  if (kSys) st_relaxed_sys(p, v); else st_relaxed_gpu(p, v);
 }
 template <bool kSys>
 __device__ __forceinline__ void fence_rel() {
@@ -392,12 +402,14 @@ __global__ void __launch_bounds__(kWsThreads) push_ws_kernel(PushArgs a0) {
   }
 }
 
-// zero-copy publication (publish_kernel; fused into recv_kernel by the step driver)
-__device__ __forceinline__ void publish_body(const PublishArgs& a) {
-  const uint64_t t0 = globaltimer();
-  if (a.need_credit && !wait_geq(a.credit, a.need_credit, t0 + a.timeout_ns)) {
+// zero-copy publication (publish_kernel; fused into recv_kernel by the step driver).
+// Header phase: wait for the slot's credit, write the 64-B header into the receiver's slot.
+// Flag phase: st.release.sys of the header flag (cumulative over the header and over the
+// producer's writes to the buffer).  false = the credit wait timed out (error latched).
+__device__ __forceinline__ bool publish_header(const PublishArgs& a) {
+  if (a.need_credit && !wait_geq(a.credit, a.need_credit, globaltimer() + a.timeout_ns)) {
     latch(a.err, PPC_ERR_TIMEOUT, a.seq, a.dir);
-    return;
+    return false;
   }
   SlotHeader h = {};
   h.magic = kMagic;
@@ -413,11 +425,18 @@ __device__ __forceinline__ void publish_body(const PublishArgs& a) {
   uint4* hd = reinterpret_cast<uint4*>(a.hdr);
 #pragma unroll
   for (int j = 0; j < 4; ++j) st_data(hd + j, hs[j]);
-  st_release_sys(a.hdr_flag, a.seq);   // cumulative: the producer's writes to the buffer too
+  return true;
+}
+__device__ __forceinline__ void publish_flag(const PublishArgs& a, uint64_t t0) {
+  st_release_sys(a.hdr_flag, a.seq);
   if (a.rec) {
     fill_record(a.rec, (long long)t0, a.rec_src, a.rec_dst, (int)a.dir, 0, a.seq, a.mb, a.bytes);
     a.rec->t_end_ns = (long long)globaltimer();
   }
+}
+__device__ __forceinline__ void publish_body(const PublishArgs& a) {
+  const uint64_t t0 = globaltimer();
+  if (publish_header(a)) publish_flag(a, t0);
 }
 
 // ---------------------------------------------------------------- K10: recv + copy-out
@@ -434,7 +453,15 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(RecvArgs a0) {
     s_zc_src = nullptr;
     if (a.rec && blockIdx.x == 0)
       fill_record(a.rec, (long long)t0, a.rec_src, a.rec_dst, -1, 1, a.seq, a.mb, a.bytes);
-    if (!wait_geq<kSys>(a.hdr_flag, a.seq, deadline)) {
+    // fused publication, header phase: written now (the slot is free once its credit is
+    // in), so its NVLink round trip overlaps this receive; the system fence orders it
+    // before the flag the last CTA releases (ordered after us through the done counter)
+    if (a.has_pub && blockIdx.x == 0) {
+      if (!publish_header(resolve(a.pub))) fail = 1;
+      __threadfence_system();
+    }
+    if (fail) {
+    } else if (!wait_geq<kSys>(a.hdr_flag, a.seq, deadline)) {
       latch(a.err, PPC_ERR_TIMEOUT, a.seq, 0x100u);
       fail = 1;
     } else {
@@ -483,9 +510,24 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(RecvArgs a0) {
     if (atomicAdd(a.done, 1u) == gridDim.x - 1) {
       *a.done = 0;                 // next use of this slot is stream-ordered after us
       __threadfence();
-      st_rel<kSys>(a.peer_credit, a.seq);
+      if (a.has_pub) {
+        // one system fence, then two relaxed stores: the next op's header flag first (it
+        // is on the critical path), then our credit.  A second release would wait for the
+        // first store's NVLink acknowledgement.
+        const PublishArgs p = resolve(a.pub);
+        const uint64_t t0 = globaltimer();
+        fence_acq_rel_sys();
+        st_relaxed_sys(p.hdr_flag, p.seq);
+        st_relaxed<kSys>(a.peer_credit, a.seq);
+        if (p.rec) {
+          fill_record(p.rec, (long long)t0, p.rec_src, p.rec_dst, (int)p.dir, 0, p.seq, p.mb,
+                      p.bytes);
+          p.rec->t_end_ns = (long long)globaltimer();
+        }
+      } else {
+        st_rel<kSys>(a.peer_credit, a.seq);
+      }
       if (a.rec) a.rec->t_end_ns = (long long)globaltimer();
-      if (a.has_pub) publish_body(resolve(a.pub));   // the next op's zero-copy send
     }
   }
 }

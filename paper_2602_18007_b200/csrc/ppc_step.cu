@@ -129,7 +129,7 @@ struct Stepper {
 
   bool done() const { return i == ops.size(); }
 
-  // before `st` writes rbuf / obuf [d][bi]: wait for a pending device->host read of it
+  // before stream q writes rbuf / obuf [d][bi]: wait for a pending device->host read of it
   ppc_status_t before_write(int kind, int d, int bi, cudaStream_t q) {
     StepBufs& sb = c->sb;
     bool* pend = kind == 1 ? &sb.dpend_r[d][bi] : &sb.dpend_o[d][bi];
