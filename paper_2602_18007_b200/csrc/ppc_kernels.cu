@@ -31,9 +31,57 @@ __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// A PDL dependent may be resident before its predecessor ends, and CTAs of it that do not
+// fit yet stay pending.  A spinning transport kernel must never be pending behind its
+// predecessor: pending CTAs can hold up other kernels on the GPU (measured: a bidirectional
+// zero-copy stream of 128-CTA receives timed out when a receive grid could not be resident
+// next to the one before it), and the kernel a spinning predecessor waits for may be the
+// peer's.  So a spinning kernel gets PDL only if two of its grids fit on the GPU at once
+// (occupancy x SMs >= 2 x grid); kernels that never spin (copy, 1-thread kernels) always.
+// CTAs of kernel k (block threads) that can be resident on the current GPU at once
+// (occupancy x SMs), cached; 0 if unknown.
+template <typename... KArgs>
+unsigned resident_capacity(void (*k)(KArgs...), unsigned block) {
+  struct Entry { const void* k; unsigned block; int dev, cap; };
+  static thread_local Entry cache[16];
+  static thread_local int used = 0;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  for (int i = 0; i < used; ++i)
+    if (cache[i].k == (const void*)k && cache[i].block == block && cache[i].dev == dev)
+      return (unsigned)cache[i].cap;
+  int per_sm = 0, sms = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, (int)block, 0) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  const Entry e{(const void*)k, block, dev, per_sm * sms};
+  cache[used < 16 ? used++ : 15] = e;
+  return (unsigned)e.cap;
+}
+template <typename... KArgs>
+bool pdl_fits(void (*k)(KArgs...), unsigned grid, unsigned block) {
+  return 2 * grid <= resident_capacity(k, block);
+}
+// A spinning grid must be resident as a whole: CTAs left pending behind it can hold up the
+// kernels its peer is waiting for (see above).  Grids are grid-strided, so any size works.
+template <typename... KArgs>
+int fit_grid(void (*k)(KArgs...), int grid, unsigned block) {
+  const unsigned cap = resident_capacity(k, block);
+  return (cap && (unsigned)grid > cap) ? (int)cap : grid;
+}
+// Cross-GPU spinning receives (and their PDL successor) must also leave SMs free for the
+// 1-thread publication / credit kernels the peer is waiting on.  Measured (2 x B200,
+// tools/zc_bidir.py, profiles/r47_zc_bidir.log): a bidirectional zero-copy stream runs with
+// 64-CTA receive grids (+ the PDL successor = 128 CTAs) and stalls until the timeout as
+// soon as the receive CTAs in flight exceed the SM count (96 + 96, 128 + 128, 256), although
+// the occupancy calculator allows two of these CTAs per SM.  64 CTAs pull at full speed.
+constexpr int kMaxSpinGrid = 64;
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(void (*k)(KArgs...), unsigned grid, unsigned block, cudaStream_t s,
-                     Args... args) {
+                     bool pdl, Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
@@ -43,7 +91,7 @@ cudaError_t launch_k(void (*k)(KArgs...), unsigned grid, unsigned block, cudaStr
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = g_pdl ? 1 : 0;
+  cfg.numAttrs = (g_pdl && pdl) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
@@ -440,8 +488,41 @@ __device__ __forceinline__ void publish_body(const PublishArgs& a) {
 }
 
 // ---------------------------------------------------------------- K10: recv + copy-out
-template <bool kSys>
-__global__ void __launch_bounds__(kThreads) recv_kernel(RecvArgs a0) {
+// Fused publication.  Its arguments are read from the grid-constant parameter space right
+// where they are used, so none of them stays live in registers across the copy loop
+// (a local copy of them had pushed the kernel to 110 registers, one CTA per SM).
+__device__ __forceinline__ bool fused_publish_header(const PublishArgs* p0) {
+  const bool ok = publish_header(resolve(*p0));
+  __threadfence_system();
+  return ok;
+}
+// one system fence, then two relaxed stores: the next op's header flag first (it is on the
+// critical path), then this receive's credit.  A second release would wait for the first
+// store's NVLink acknowledgement.
+__device__ __forceinline__ void fused_publish_flag(const PublishArgs* p0, uint64_t* credit,
+                                                  uint64_t seq) {
+  uint64_t pseq = p0->seq;
+  uint64_t* flag = p0->hdr_flag;
+  if (p0->sr.base) {                  // graph replay: resolve seq and slot (as resolve())
+    pseq += *p0->sr.base;
+    flag += pseq % p0->sr.K;
+  }
+  const uint64_t t0 = globaltimer();
+  fence_acq_rel_sys();
+  st_relaxed_sys(flag, pseq);
+  st_relaxed_sys(credit, seq);
+  if (ppc_record_t* r = p0->rec) {
+    fill_record(r, (long long)t0, p0->rec_src, p0->rec_dst, (int)p0->dir, 0, pseq, p0->mb,
+                p0->bytes);
+    r->t_end_ns = (long long)globaltimer();
+  }
+}
+
+// kPub: the variant with the fused publication (step driver, terminal receives of a
+// comm-only PP2 step); it needs 88 registers (one CTA per SM), so the plain variant, which
+// shares SMs with the push kernels of deeper pipelines, is kept at 64.
+template <bool kSys, bool kPub>
+__global__ void __launch_bounds__(kThreads) recv_kernel(const __grid_constant__ RecvArgs a0) {
   pdl_enter();
   const RecvArgs a = resolve(a0);
   __shared__ const uint8_t* s_zc_src;   // zero-copy: the sender's buffer, mapped here
@@ -456,10 +537,7 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(RecvArgs a0) {
     // fused publication, header phase: written now (the slot is free once its credit is
     // in), so its NVLink round trip overlaps this receive; the system fence orders it
     // before the flag the last CTA releases (ordered after us through the done counter)
-    if (a.has_pub && blockIdx.x == 0) {
-      if (!publish_header(resolve(a.pub))) fail = 1;
-      __threadfence_system();
-    }
+    if (kPub && blockIdx.x == 0 && !fused_publish_header(&a0.pub)) fail = 1;
     if (fail) {
     } else if (!wait_geq<kSys>(a.hdr_flag, a.seq, deadline)) {
       latch(a.err, PPC_ERR_TIMEOUT, a.seq, 0x100u);
@@ -510,20 +588,8 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(RecvArgs a0) {
     if (atomicAdd(a.done, 1u) == gridDim.x - 1) {
       *a.done = 0;                 // next use of this slot is stream-ordered after us
       __threadfence();
-      if (a.has_pub) {
-        // one system fence, then two relaxed stores: the next op's header flag first (it
-        // is on the critical path), then our credit.  A second release would wait for the
-        // first store's NVLink acknowledgement.
-        const PublishArgs p = resolve(a.pub);
-        const uint64_t t0 = globaltimer();
-        fence_acq_rel_sys();
-        st_relaxed_sys(p.hdr_flag, p.seq);
-        st_relaxed<kSys>(a.peer_credit, a.seq);
-        if (p.rec) {
-          fill_record(p.rec, (long long)t0, p.rec_src, p.rec_dst, (int)p.dir, 0, p.seq, p.mb,
-                      p.bytes);
-          p.rec->t_end_ns = (long long)globaltimer();
-        }
+      if (kPub) {
+        fused_publish_flag(&a0.pub, a.peer_credit, a.seq);
       } else {
         st_rel<kSys>(a.peer_credit, a.seq);
       }
@@ -591,7 +657,8 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(GatherArgs a) {
 }
 
 cudaError_t launch_gather(const GatherArgs& a, int grid, cudaStream_t s) {
-  return launch_k(gather_kernel, grid, kThreads, s, a);
+  grid = fit_grid(gather_kernel, std::min(grid, kMaxSpinGrid), kThreads);
+  return launch_k(gather_kernel, grid, kThreads, s, pdl_fits(gather_kernel, grid, kThreads), a);
 }
 
 // ---------------------------------------------------------------- zero-copy publication
@@ -604,7 +671,7 @@ __global__ void publish_kernel(PublishArgs a0) {
 }
 
 cudaError_t launch_publish(const PublishArgs& a, cudaStream_t s) {
-  return launch_k(publish_kernel, 1, 1, s, a);
+  return launch_k(publish_kernel, 1, 1, s, true, a);
 }
 
 // ---------------------------------------------------------------- K12: CE signalling
@@ -719,21 +786,31 @@ __global__ void __launch_bounds__(kThreads, 2) copy_kernel(uint8_t* dst, const u
 cudaError_t launch_copy(void* dst, const void* src, uint64_t bytes, uint64_t chunk, int grid,
                         cudaStream_t s) {
   if (bytes == 0) return cudaSuccess;
-  return launch_k(copy_kernel, grid, kThreads, s, static_cast<uint8_t*>(dst),
+  return launch_k(copy_kernel, grid, kThreads, s, true, static_cast<uint8_t*>(dst),
                   static_cast<const uint8_t*>(src), bytes, chunk);
 }
 
 cudaError_t launch_wait_credit(const uint64_t* credit, uint64_t target, ErrWord* err,
                                uint64_t timeout_ns, cudaStream_t s, const uint64_t* seq_base) {
-  return launch_k(wait_credit_kernel, 1, 1, s, credit, target, err, timeout_ns, seq_base);
+  return launch_k(wait_credit_kernel, 1, 1, s, true, credit, target, err, timeout_ns, seq_base);
 }
 
 cudaError_t launch_push(const PushArgs& a, int grid, bool sys, bool ws, cudaStream_t s) {
-  if (ws) return launch_k(sys ? push_ws_kernel<true> : push_ws_kernel<false>, grid, kWsThreads, s, a);
-  return launch_k(sys ? push_kernel<true> : push_kernel<false>, grid, kThreads, s, a);
+  if (ws) {
+    auto k = sys ? push_ws_kernel<true> : push_ws_kernel<false>;
+    grid = fit_grid(k, grid, kWsThreads);
+    return launch_k(k, grid, kWsThreads, s, pdl_fits(k, grid, kWsThreads), a);
+  }
+  auto k = sys ? push_kernel<true> : push_kernel<false>;
+  grid = fit_grid(k, grid, kThreads);
+  return launch_k(k, grid, kThreads, s, pdl_fits(k, grid, kThreads), a);
 }
 cudaError_t launch_recv(const RecvArgs& a, int grid, bool sys, cudaStream_t s) {
-  return launch_k(sys ? recv_kernel<true> : recv_kernel<false>, grid, kThreads, s, a);
+  auto k = a.has_pub ? (sys ? recv_kernel<true, true> : recv_kernel<false, true>)
+                     : (sys ? recv_kernel<true, false> : recv_kernel<false, false>);
+  if (sys) grid = std::min(grid, kMaxSpinGrid);
+  grid = fit_grid(k, grid, kThreads);
+  return launch_k(k, grid, kThreads, s, pdl_fits(k, grid, kThreads), a);
 }
 cudaError_t launch_ce_head(const CeHeadArgs& a, cudaStream_t s) {
   ce_head_kernel<<<1, 1, 0, s>>>(a);
@@ -756,7 +833,8 @@ cudaError_t preload_kernels() {
   const void* fns[] = {
       (const void*)push_kernel<true>,      (const void*)push_kernel<false>,
       (const void*)push_ws_kernel<true>,   (const void*)push_ws_kernel<false>,
-      (const void*)recv_kernel<true>,      (const void*)recv_kernel<false>,
+      (const void*)recv_kernel<true, false>, (const void*)recv_kernel<false, false>,
+      (const void*)recv_kernel<true, true>,  (const void*)recv_kernel<false, true>,
       (const void*)gather_kernel,          (const void*)publish_kernel,
       (const void*)ce_head_kernel,         (const void*)ce_flags_kernel,
       (const void*)wait_credit_kernel,     (const void*)set_seq_kernel,

@@ -219,6 +219,41 @@ def case_zc(rank, world):
     return comm
 
 
+def case_zc_bidir_stream(rank, world):
+    """Both directions at once, a stream of zero-copy messages per direction, every receive
+    of a direction enqueued before its sends (bench_sweep's bidir mode), with 128- and
+    256-CTA receive grids requested.  Regression for a stall until the timeout when the
+    spinning receive CTAs in flight exceeded the SM count and the peer's publication kernels
+    could no longer be scheduled (libppc now caps cross-GPU receive grids at 64 CTAs,
+    profiles/r47_zc_bidir.log)."""
+    n, N = 32 << 20, 8
+    cfg = ppc.make_config(pp=world, max_msg_bytes=n, chunk_bytes=128 << 10,
+                          timeout_ns=5_000_000_000)      # 256 chunks: grids up to 256 CTAs
+    comm = ppc.connect_distributed(cfg, rank, world, rank, with_nccl=False)
+    src = buf(n)
+    ppc.fill_payload(src, n, 42, 0, 0, rank, 0)
+    ppc.register_tensors(comm, [src])
+    dst = buf(n)
+    s_send, s_recv = torch.cuda.Stream(), torch.cuda.Stream()
+    d_out = ppc.FWD if rank == 0 else ppc.BWD
+    d_in = ppc.BWD if rank == 0 else ppc.FWD
+    for rep in range(4):
+        # 128 CTAs: two receive grids fit (PDL on); 256: they do not (PDL off for them)
+        os.environ["PPC_RECV_CTAS"] = "128" if rep < 2 else "256"
+        torch.cuda.synchronize()
+        dist.barrier()
+        for i in range(N):
+            comm.recv(d_in, dst, n, mb=rep * N + i, stream=s_recv)
+        for i in range(N):
+            comm.send(d_out, src, n, mb=rep * N + i, stream=s_send)
+        torch.cuda.synchronize()
+        assert comm.poll() == 0, comm.error_info()
+    want = P.payload_bytes(42, 0, 0, 1 - rank, 0, n)
+    assert np.array_equal(host(dst)[:n], want)
+    os.environ.pop("PPC_RECV_CTAS")
+    return comm
+
+
 def case_graph(rank, world, zc=False):
     """A 1F1B step captured into a CUDA graph across processes (device-side sequence bases):
     XOR step graph launches interleaved with eager steps; then an identity step whose X / G
@@ -412,6 +447,8 @@ def main():
     elif case == "zc_side":              # publication on the send stream (PPC_ZC_SIDE=1)
         os.environ["PPC_ZC_SIDE"] = "1"
         comm = case_zc(rank, world)
+    elif case == "zc_bidir_stream":
+        comm = case_zc_bidir_stream(rank, world)
     elif case == "graph":
         comm = case_graph(rank, world)
     elif case == "fullsize":
