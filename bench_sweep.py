@@ -35,7 +35,8 @@ def parse():
     ap.add_argument("--sm", default="16:1M,32:1M,64:1M,32:256K,64:256K,128:256K,32:4M")
     ap.add_argument("--ce", default="1,2,4,8")
     ap.add_argument("--pull", default="", help="PULL engine specs cta:chunk, e.g. 32:1M,64:1M")
-    ap.add_argument("--zc", default="", help="zero-copy specs recv_ctas:chunk, e.g. 64:256K")
+    ap.add_argument("--zc", default="", help="zero-copy specs recv_ctas:chunk[:a], e.g. 64:256K "
+                                             "(:a = cfg.zc_async, sends complete at publication)")
     ap.add_argument("--modes", default="uni,bidir")
     ap.add_argument("--comparators", default="nccl,ce_copy,gloo")
     ap.add_argument("--reps", type=int, default=5)
@@ -208,13 +209,16 @@ def main():
         dist.barrier()
         comm.destroy()
     for spec in [x for x in a.zc.split(",") if x]:
-        rc, chunk = spec.split(":")
+        parts = spec.split(":")            # recv_ctas:chunk[:a]  (a = cfg.zc_async)
+        rc, chunk = parts[0], parts[1]
+        zc_async = len(parts) > 2 and parts[2] == "a"
         os.environ["PPC_RECV_CTAS"] = rc
-        cfg = ppc.make_config(pp=world, max_msg_bytes=maxn, chunk_bytes=size_of(chunk))
+        cfg = ppc.make_config(pp=world, max_msg_bytes=maxn, chunk_bytes=size_of(chunk),
+                              zc_async=int(zc_async))
         comm = ppc.connect_distributed(cfg, rank, world, torch.cuda.current_device(),
                                        with_nccl=False)
-        bench_ppc(comm, rank, sizes, modes, f"ppc_zerocopy_recv{rc}_chunk{chunk}", a.reps, fh,
-                  zc=True)
+        label = f"ppc_zerocopy{'_async' if zc_async else ''}_recv{rc}_chunk{chunk}"
+        bench_ppc(comm, rank, sizes, modes, label, a.reps, fh, zc=True)
         os.environ.pop("PPC_RECV_CTAS")
         dist.barrier()
         comm.disconnect()

@@ -98,6 +98,10 @@ typedef struct {
   int trace;                    /* bit 0: %globaltimer records per transfer (ppc_trace);
                                    bit 1: CUDA-event pair around every send / recv launch on
                                    its stream (ppc_kernel_times)                               */
+  int zc_async;                 /* 1: a zero-copy ppc_pp_send completes at publication, so
+                                   consecutive sends on one stream overlap; the caller keeps
+                                   the buffer unchanged until ppc_pp_wait_consumed (like an
+                                   MPI_Isend / MPI_Wait pair).  0: rendezvous (default)        */
 } ppc_config_t;
 
 typedef struct ppc_comm ppc_comm_t;
@@ -185,7 +189,9 @@ ppc_status_t ppc_pp_wait_consumed(ppc_comm_t* c, ppc_dir_t d, cudaStream_t s);
  * a registered range moves no data on the sender: it publishes (segment, offset) in the
  * receiver's slot header and the receiver's CTAs LOAD the payload over NVLink straight into
  * their user buffer (one pass, no ring copy).  The send completes on its stream only when
- * the receiver has consumed the message (rendezvous), so the buffer may be reused after it.
+ * the receiver has consumed the message (rendezvous), so the buffer may be reused after it
+ * — unless cfg.zc_async, where it completes at publication and ppc_pp_wait_consumed marks
+ * the point after which the buffers of all earlier sends may be reused.
  * Blobs of non-neighbours are accepted and ignored.  Up to 256 registrations per comm. */
 #define PPC_REG_BLOB_BYTES 128
 ppc_status_t ppc_register(ppc_comm_t* c, const void* ptr, size_t bytes, void* blob,

@@ -48,7 +48,7 @@ class Config(C.Structure):
     _fields_ = [("tp", C.c_int), ("pp", C.c_int), ("dp", C.c_int),
                 ("max_msg_bytes", C.c_size_t), ("ring_slots", C.c_int), ("channels", C.c_int),
                 ("chunk_bytes", C.c_size_t), ("engine", C.c_int), ("cta_per_channel", C.c_int),
-                ("timeout_ns", C.c_ulonglong), ("trace", C.c_int)]
+                ("timeout_ns", C.c_ulonglong), ("trace", C.c_int), ("zc_async", C.c_int)]
 
 
 class Op(C.Structure):
@@ -151,9 +151,9 @@ def _stream(s):
 
 def make_config(tp=1, pp=2, dp=1, max_msg_bytes=32 << 20, ring_slots=0, channels=1,
                 chunk_bytes=1 << 20, engine=ENGINE_SM, cta_per_channel=0, timeout_ns=0,
-                trace=0) -> Config:
+                trace=0, zc_async=0) -> Config:
     return Config(tp, pp, dp, max_msg_bytes, ring_slots, channels, chunk_bytes, engine,
-                  cta_per_channel, timeout_ns, trace)
+                  cta_per_channel, timeout_ns, trace, zc_async)
 
 
 def schedule_1f1b(S: int, s: int, M: int):

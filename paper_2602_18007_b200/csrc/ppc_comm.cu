@@ -500,7 +500,10 @@ ppc_status_t ppc_impl_send_ex(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_
     ZcSend z;
     fill_publish(c, d, seq, need, bytes, mb, zc_seg, zc_off, rec, &z);
     CK(launch_publish(z.p, s));
-    if (ppc_status_t ws = ppc_impl_zc_commit(c, z, s, s_wait)) return ws;
+    // public call with cfg.zc_async: complete at publication (ppc_pp_wait_consumed waits)
+    const bool async = c->cfg.zc_async && s_wait == s;
+    if (!async)
+      if (ppc_status_t ws = ppc_impl_zc_commit(c, z, s, s_wait)) return ws;
   } else if (c->cfg.engine != PPC_ENGINE_CE || bytes == 0) {  // SM push, or PULL's staging
     PushArgs a{};
     a.src = static_cast<const uint8_t*>(buf);

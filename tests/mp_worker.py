@@ -254,6 +254,37 @@ def case_zc_bidir_stream(rank, world):
     return comm
 
 
+def case_zc_async(rank, world):
+    """cfg.zc_async: zero-copy sends complete at publication, so a stream of sends overlaps;
+    ppc_pp_wait_consumed marks buffer reuse.  Distinct registered buffers per message, both
+    directions at once, ragged sizes; every message byte-exact and in order."""
+    sizes = [1, 4096 + 3, 3 * (256 << 10) + 5, 8 << 20, 5 << 20]
+    cfg = ppc.make_config(pp=world, max_msg_bytes=8 << 20, chunk_bytes=256 << 10, zc_async=1)
+    comm = ppc.connect_distributed(cfg, rank, world, rank, with_nccl=False)
+    src = [buf(n) for n in sizes]
+    for i, (b, n) in enumerate(zip(src, sizes)):
+        ppc.fill_payload(b, n, 42, 0, 0, rank, i)
+    ppc.register_tensors(comm, src)
+    outs = [buf(n) for n in sizes]
+    s_send, s_recv = torch.cuda.Stream(), torch.cuda.Stream()
+    d_out = ppc.FWD if rank == 0 else ppc.BWD
+    d_in = ppc.BWD if rank == 0 else ppc.FWD
+    for rep in range(2):
+        for i, n in enumerate(sizes):
+            comm.recv(d_in, outs[i], n, mb=rep * len(sizes) + i, stream=s_recv)
+        for i, n in enumerate(sizes):
+            comm.send(d_out, src[i], n, mb=rep * len(sizes) + i, stream=s_send)
+        comm.wait_consumed(d_out, s_send)
+        torch.cuda.synchronize()
+        assert comm.poll() == 0, comm.error_info()
+        for i, n in enumerate(sizes):
+            assert np.array_equal(host(outs[i])[:n], P.payload_bytes(42, 0, 0, 1 - rank, i, n)), i
+            outs[i].zero_()
+        torch.cuda.synchronize()
+        dist.barrier()
+    return comm
+
+
 def case_graph(rank, world, zc=False):
     """A 1F1B step captured into a CUDA graph across processes (device-side sequence bases):
     XOR step graph launches interleaved with eager steps; then an identity step whose X / G
@@ -449,6 +480,8 @@ def main():
         comm = case_zc(rank, world)
     elif case == "zc_bidir_stream":
         comm = case_zc_bidir_stream(rank, world)
+    elif case == "zc_async":
+        comm = case_zc_async(rank, world)
     elif case == "graph":
         comm = case_graph(rank, world)
     elif case == "fullsize":

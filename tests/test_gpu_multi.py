@@ -57,6 +57,10 @@ def test_zero_copy_bidirectional_stream():
     _run("zc_bidir_stream", 2)
 
 
+def test_zero_copy_async_sends():
+    _run("zc_async", 2)
+
+
 @pytest.mark.parametrize("n", [2, 4])
 def test_step_cuda_graph(n):
     _run("graph", n)
