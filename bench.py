@@ -377,8 +377,14 @@ def main():
                             f"(step {ms_instr / args.steps:.3f} ms instrumented vs {ms_step:.3f} plain)",
             "step_aggregate": {"bytes_per_step": alg * len(push_ms) / max(1, args.steps),
                                "achieved": alg * len(push_ms) / (ms_instr * 1e-3) / 1e9,
+                               "achieved_plain": alg * len(push_ms) / max(1, args.steps)
+                                                 / (ms_step * 1e-3) / 1e9,
+                               "frac_plain": alg * len(push_ms) / max(1, args.steps)
+                                             / (ms_step * 1e-3) / 1e9 / peak,
                                "note": "this process's transfer launches of the step (both "
-                                       "directions, concurrent) over the instrumented step time"},
+                                       "directions, concurrent) over the instrumented step "
+                                       "time (achieved) and over the un-instrumented headline "
+                                       "step time (achieved_plain)"},
             "recv_avg_launch_us": (statistics.mean(recv_ms) * 1e3) if recv_ms else None}
     # launches of the dominant kernel overlap (the F and B transfers of a 1F1B step run
     # concurrently and share the bandwidth), so per-launch "achieved" is ~1/concurrency of

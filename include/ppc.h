@@ -272,6 +272,9 @@ ppc_status_t ppc_set_trace(ppc_comm_t* c, int trace);
 ppc_status_t ppc_disconnect(ppc_comm_t* c);        /* phase 1: close peer handles, NCCL    */
 ppc_status_t ppc_destroy(ppc_comm_t* c);           /* phase 2 (after a caller barrier)     */
 const char* ppc_status_str(ppc_status_t st);
+/* sizeof of the ABI structs, for bindings to check their layouts: which = 0 ppc_config_t,
+ * 1 ppc_step_t, 2 ppc_record_t, 3 ppc_op_t; 0 for any other value. */
+size_t ppc_struct_size(int which);
 
 /* ---- test/bench kernels (K14); not part of the transfer path --------------------------- */
 /* Fill `bytes` of device buffer with the synth/payload.py SplitMix64 stream of key

@@ -87,6 +87,16 @@ int find_reg(const ppc_comm* c, const void* p, size_t bytes, uint64_t* off) {
 
 extern "C" {
 
+size_t ppc_struct_size(int which) {
+  switch (which) {
+    case 0: return sizeof(ppc_config_t);
+    case 1: return sizeof(ppc_step_t);
+    case 2: return sizeof(ppc_record_t);
+    case 3: return sizeof(ppc_op_t);
+  }
+  return 0;
+}
+
 const char* ppc_status_str(ppc_status_t st) {
   switch (st) {
     case PPC_OK: return "PPC_OK";

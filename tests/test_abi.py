@@ -29,6 +29,15 @@ def test_exports_every_declared_symbol():
         assert hasattr(lib, n), n
 
 
+def test_struct_layouts_match_the_binding():
+    lib = ctypes.CDLL(ppc.lib_path())
+    lib.ppc_struct_size.restype = ctypes.c_size_t
+    lib.ppc_struct_size.argtypes = [ctypes.c_int]
+    for which, cls in enumerate([ppc.Config, ppc.Step, ppc.Record, ppc.Op]):
+        assert lib.ppc_struct_size(which) == ctypes.sizeof(cls), cls.__name__
+    assert lib.ppc_struct_size(7) == 0
+
+
 def test_schedule_matches_oracle():
     for S in range(1, 9):
         for s in range(S):
