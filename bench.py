@@ -347,8 +347,12 @@ def main():
         dist.all_reduce(t)
         n_launch = int(t.item())
 
-    # dominant kernel: the push (peer write / HBM ring write)
-    avg_push_ms = statistics.mean(push_ms) if push_ms else float("nan")
+    # dominant kernel: the one that moves the bytes — N=1: the hand-off copy; N>=2 zero-copy:
+    # the receiver's NVLink pull (recv_kernel; its launch also spans the wait for the peer's
+    # publication); N>=2 ring: the SM push
+    zc_dom = distributed and bool(args.zc)
+    dom_ms = recv_ms if zc_dom else push_ms
+    avg_push_ms = statistics.mean(dom_ms) if dom_ms else float("nan")
     avg_push_ms = max_over_ranks(avg_push_ms)
     peaks = measured_peaks()
     if distributed:
@@ -362,35 +366,37 @@ def main():
         peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
     achieved = alg / (avg_push_ms * 1e-3) / 1e9
     if not distributed:
-        kname = "ppc::copy_kernel (virtual-stage single-copy hand-off)"
-    elif args.zc:
-        kname = ("zero-copy send op: publish_kernel -> receiver recv_kernel NVLink pull -> "
-                 "credit (CUDA events on the sender stream bracket the whole transfer)")
+        kname, tkey = "ppc::copy_kernel (virtual-stage single-copy hand-off)", "copy_n1"
+    elif zc_dom:
+        kname = ("ppc::recv_kernel (zero-copy NVLink pull into the user buffer; CUDA events "
+                 "on its stream, so the launch time includes the wait for the publication)")
+        tkey = "recv_n2"
     else:
-        kname = "ppc::push_ws_kernel (SM push over NVLink)"
+        kname, tkey = "ppc::push_ws_kernel (SM push over NVLink)", "push_n2"
     roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
-            "frac": achieved / peak, "traffic": ncu_traffic("push_n%d" % min(world, 2)),
+            "frac": achieved / peak, "traffic": ncu_traffic(tkey),
             "kernel": kname, "alg_bytes_per_launch": alg,
-            "avg_launch_us": avg_push_ms * 1e3, "launches_timed": len(push_ms),
+            "avg_launch_us": avg_push_ms * 1e3, "launches_timed": len(dom_ms),
             "peak_source": peak_src,
             "timed_region": "second pass of the same K steps with per-launch CUDA events "
                             f"(step {ms_instr / args.steps:.3f} ms instrumented vs {ms_step:.3f} plain)",
-            "step_aggregate": {"bytes_per_step": alg * len(push_ms) / max(1, args.steps),
-                               "achieved": alg * len(push_ms) / (ms_instr * 1e-3) / 1e9,
-                               "achieved_plain": alg * len(push_ms) / max(1, args.steps)
+            "step_aggregate": {"bytes_per_step": alg * len(dom_ms) / max(1, args.steps),
+                               "achieved": alg * len(dom_ms) / (ms_instr * 1e-3) / 1e9,
+                               "achieved_plain": alg * len(dom_ms) / max(1, args.steps)
                                                  / (ms_step * 1e-3) / 1e9,
-                               "frac_plain": alg * len(push_ms) / max(1, args.steps)
+                               "frac_plain": alg * len(dom_ms) / max(1, args.steps)
                                              / (ms_step * 1e-3) / 1e9 / peak,
                                "note": "this process's transfer launches of the step (both "
                                        "directions, concurrent) over the instrumented step "
                                        "time (achieved) and over the un-instrumented headline "
                                        "step time (achieved_plain)"},
+            "send_avg_launch_us": (statistics.mean(push_ms) * 1e3) if push_ms else None,
             "recv_avg_launch_us": (statistics.mean(recv_ms) * 1e3) if recv_ms else None}
     # launches of the dominant kernel overlap (the F and B transfers of a 1F1B step run
     # concurrently and share the bandwidth), so per-launch "achieved" is ~1/concurrency of
     # what the kernel class moves; report the measured overlap beside it
-    if push_ms and ms_instr > 0:
-        conc = sum(push_ms) / ms_instr       # this process's launches (all its stages)
+    if dom_ms and ms_instr > 0:
+        conc = sum(dom_ms) / ms_instr        # this process's launches (all its stages)
         roof["concurrency"] = conc
         roof["frac_x_concurrency"] = roof["frac"] * conc
     if distributed and args.zc and recv_recs:
