@@ -121,7 +121,10 @@ typedef int (*ppc_stage_fn)(void* user, int mb, const void* in, void* out,
                             size_t in_bytes, size_t out_bytes, cudaStream_t s);
 
 /* One 1F1B step (ppc_step_1f1b).  fwd/bwd NULL => identity stage (out = in).  x/g/y/dx
- * entries may be host or device pointers (host => copied inside the call, on stream). */
+ * entries may be host or device pointers.  Host (pinned for full speed) => copied inside
+ * the step: inputs are staged into the step buffers on an internal host->device stream that
+ * runs ahead as soon as a staging buffer is free, outputs leave on an internal
+ * device->host stream; both complete within the step's stream order on `s`. */
 typedef struct {
   int M;                         /* micro-batches                                            */
   size_t fwd_bytes, bwd_bytes;   /* boundary activation / gradient bytes per micro-batch      */

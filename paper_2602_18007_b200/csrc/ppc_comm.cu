@@ -953,12 +953,15 @@ ppc_status_t ppc_destroy(ppc_comm_t* c) {
     if (sb.xdone) cudaEventDestroy(sb.xdone);
     if (sb.xq) cudaStreamDestroy(sb.xq);
     if (sb.ds) cudaStreamDestroy(sb.ds);
+    if (sb.hs) cudaStreamDestroy(sb.hs);
     if (sb.dgo) cudaEventDestroy(sb.dgo);
     if (sb.djoin) cudaEventDestroy(sb.djoin);
     for (int d = 0; d < 2; ++d)
       for (int i = 0; i < 2; ++i) {
         if (sb.dfree_r[d][i]) cudaEventDestroy(sb.dfree_r[d][i]);
         if (sb.dfree_o[d][i]) cudaEventDestroy(sb.dfree_o[d][i]);
+        if (sb.hdone[d][i]) cudaEventDestroy(sb.hdone[d][i]);
+        if (sb.rlast[d][i]) cudaEventDestroy(sb.rlast[d][i]);
       }
     for (int d = 0; d < 2; ++d) if (sb.join[d]) cudaEventDestroy(sb.join[d]);
     for (int d = 0; d < 2; ++d) {

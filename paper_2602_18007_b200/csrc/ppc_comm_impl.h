@@ -109,6 +109,12 @@ struct StepBufs {
   cudaStream_t ds = nullptr;
   cudaEvent_t dgo = nullptr, djoin = nullptr, dfree_r[2][2] = {}, dfree_o[2][2] = {};
   bool dpend_r[2][2] = {}, dpend_o[2][2] = {};
+  // host->device staging of host inputs runs ahead on hs: it waits only for the staging
+  // buffer rbuf [dir][i] to be free (rfree / rlast / cons), not for the compute stream;
+  // hdone = staged, rlast = the compute stream's last read of rbuf [dir][i] (a stage fn)
+  cudaStream_t hs = nullptr;
+  cudaEvent_t hdone[2][2] = {}, rlast[2][2] = {};
+  bool rlast_set[2][2] = {};
   cudaEvent_t rfree[2][2] = {}, ofree[2][2] = {}, ready = nullptr, join[2] = {};
   bool rpending[2][2] = {}, opending[2][2] = {};
   // direct (single-copy) mode of same-GPU virtual stages: [dir][i] of the buffer handed to

@@ -33,6 +33,7 @@ ppc_status_t ensure_bufs(ppc_comm* c, size_t bytes) {
     CK(cudaEventCreateWithFlags(&sb.dgo, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&sb.djoin, cudaEventDisableTiming));
     CK(cudaStreamCreateWithFlags(&sb.ds, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&sb.hs, cudaStreamNonBlocking));
     for (int d = 0; d < 2; ++d) {
       CK(cudaEventCreateWithFlags(&sb.join[d], cudaEventDisableTiming));
       for (int i = 0; i < 2; ++i) {
@@ -43,6 +44,8 @@ ppc_status_t ensure_bufs(ppc_comm* c, size_t bytes) {
         CK(cudaEventCreateWithFlags(&sb.cons_o[d][i], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&sb.dfree_r[d][i], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&sb.dfree_o[d][i], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&sb.hdone[d][i], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&sb.rlast[d][i], cudaEventDisableTiming));
       }
     }
   }
@@ -140,6 +143,17 @@ struct Stepper {
     return PPC_OK;
   }
 
+  // the compute stream just read `in`: if it is the staging buffer rbuf [d][bi], the next
+  // host->device staging into it (on hs) must wait for this point
+  ppc_status_t mark_read(const void* in, int d, int bi) {
+    StepBufs& sb = c->sb;
+    if (in && in == sb.rbuf[d][bi]) {
+      CK(cudaEventRecord(sb.rlast[d][bi], cs));
+      sb.rlast_set[d][bi] = true;
+    }
+    return PPC_OK;
+  }
+
   // terminal output to host memory: copy on the D2H stream (kind: 1 = src is rbuf [d][bi],
   // 2 = obuf [d][bi], 0 = a caller buffer)
   ppc_status_t d2h(void* dst, const void* src, size_t bytes, int kind, int d, int bi) {
@@ -180,14 +194,14 @@ struct Stepper {
 
   // direct mode: may the stage overwrite its buffer (kind 1 = rbuf, 2 = obuf) [d][bi]?
   // false = the receiving stage has not enqueued its copy yet (caller returns, retries).
-  bool reuse_ok(int kind, int d, int bi, ppc_status_t* err) {
+  bool reuse_ok(int kind, int d, int bi, ppc_status_t* err, cudaStream_t q = nullptr) {
     StepBufs& sb = c->sb;
     bool* held = kind == 1 ? &sb.held_r[d][bi] : &sb.held_o[d][bi];
     bool* cw = kind == 1 ? &sb.cwait_r[d][bi] : &sb.cwait_o[d][bi];
     if (*held) return false;
     if (*cw) {
       cudaEvent_t e = kind == 1 ? sb.cons_r[d][bi] : sb.cons_o[d][bi];
-      if (cudaStreamWaitEvent(cs, e, 0) != cudaSuccess) { *err = PPC_ERR_CUDA; return false; }
+      if (cudaStreamWaitEvent(q ? q : cs, e, 0) != cudaSuccess) { *err = PPC_ERR_CUDA; return false; }
       *cw = false;
     }
     return true;
@@ -266,16 +280,26 @@ struct Stepper {
           const void* const* srcs = kind == 0 ? st->x : st->g;
           in = srcs ? srcs[m] : nullptr;
           if (in && is_host_ptr(in)) {
+            // stage the host input on hs, ahead of the compute stream: wait only until the
+            // staging buffer's previous contents are consumed (send done / copied by the next
+            // virtual stage / read by this stage's fn / read by a device->host copy)
             uint8_t* r = sb.rbuf[d][bi];
+            cudaStream_t q = sb.hs;
             if (dmode) {
               ppc_status_t e = PPC_OK;
-              if (!reuse_ok(1, d, bi, &e)) return e;
+              if (!reuse_ok(1, d, bi, &e, q)) return e;
             } else if (sb.rpending[d][bi]) {
-              CK(cudaStreamWaitEvent(cs, sb.rfree[d][bi], 0));
+              CK(cudaStreamWaitEvent(q, sb.rfree[d][bi], 0));
             }
             sb.rpending[d][bi] = false;
-            if (ppc_status_t w = before_write(1, d, bi, cs)) return w;
-            CK(cudaMemcpyAsync(r, in, bytes, cudaMemcpyHostToDevice, cs));
+            if (sb.rlast_set[d][bi]) {
+              CK(cudaStreamWaitEvent(q, sb.rlast[d][bi], 0));
+              sb.rlast_set[d][bi] = false;
+            }
+            if (ppc_status_t w = before_write(1, d, bi, q)) return w;
+            CK(cudaMemcpyAsync(r, in, bytes, cudaMemcpyHostToDevice, q));
+            CK(cudaEventRecord(sb.hdone[d][bi], q));
+            CK(cudaStreamWaitEvent(cs, sb.hdone[d][bi], 0));
             in = r;
           }
         }
@@ -296,6 +320,7 @@ struct Stepper {
             uint8_t* o = sb.obuf[d][bi];
             if (ppc_status_t w = before_write(2, d, bi, cs)) return w;
             if (fn && fn(user, m, in, o, in ? bytes : 0, bytes, cs) != 0) return PPC_ERR_INVALID_ARG;
+            mark_read(in, d, bi);
             send_src = o;          // no input and no fn: scratch contents
             send_free = sb.ofree[d][bi];
             send_pending = &sb.opending[d][bi];
@@ -338,6 +363,7 @@ struct Stepper {
             if (target == o)
               if (ppc_status_t w = before_write(2, d, bi, cs)) return w;
             if (fn(user, m, in, target, in ? bytes : 0, bytes, cs) != 0) return PPC_ERR_INVALID_ARG;
+            mark_read(in, d, bi);
             if (host)
               if (ppc_status_t w = d2h(dst, o, bytes, 2, d, bi)) return w;
           } else if (dst && in && bytes && !direct) {

@@ -91,6 +91,46 @@ def case_xor(rank, world, engine, M=6):
     return comm
 
 
+def case_host(rank, world, M=6):
+    """The e2e path across processes: pinned HOST X / G in, HOST Y / DX out, XOR stage
+    functions and identity, 3 steps each (staging buffers reused behind the host->device
+    and device->host streams); middle stages (world > 2) forward zero-copy from the step
+    buffers in their arena."""
+    S = world
+    n = 3 * (256 << 10) + 321
+    cfg = ppc.make_config(pp=S, max_msg_bytes=n, chunk_bytes=256 << 10)
+    comm = ppc.connect_distributed(cfg, rank, world, rank, with_nccl=False)
+    pin = lambda a: torch.from_numpy(a.copy()).pin_memory()
+    hX = [pin(P.source_activation(42, 0, m, n)) for m in range(M)] if rank == 0 else None
+    hG = [pin(P.source_gradient(42, 0, m, n)) for m in range(M)] if rank == S - 1 else None
+    hout = [torch.zeros(n, dtype=torch.uint8).pin_memory() for _ in range(M)]
+    fctx, bctx = ppc.XorCtx(42, 0, rank, 0), ppc.XorCtx(42, 0, rank, 1)
+    mask = lambda s, d, m: P.proxy_mask(42, 0, s, d, m, n)
+    for fn in (True, False):
+        args = ppc.StepArgs(M, n, n, fwd=ppc.STAGE_XOR if fn else None,
+                            bwd=ppc.STAGE_XOR if fn else None,
+                            fwd_user=fctx if fn else None, bwd_user=bctx if fn else None,
+                            x=hX, g=hG, y=hout if rank == S - 1 else None,
+                            dx=hout if rank == 0 else None)
+        for step in range(3):
+            for t in hout:
+                t.zero_()
+            ppc.step_1f1b(comm, args, torch.cuda.current_stream())
+            torch.cuda.synchronize()
+            assert comm.poll() == 0, comm.error_info()
+            if rank in (0, S - 1):
+                for m in range(M):
+                    xs, gs = P.source_activation(42, 0, m, n), P.source_gradient(42, 0, m, n)
+                    if fn:
+                        y, g = xor_closed_form(S, m, xs, gs, mask)
+                    else:
+                        y, g = xs, gs
+                    want = y if rank == S - 1 else g
+                    assert np.array_equal(hout[m].numpy(), want), (rank, fn, step, m)
+            dist.barrier()
+    return comm
+
+
 def case_timeout(rank, world):
     cfg = ppc.make_config(pp=world, max_msg_bytes=1 << 20, timeout_ns=300_000_000)
     comm = ppc.connect_distributed(cfg, rank, world, rank, with_nccl=False)
@@ -480,6 +520,8 @@ def main():
         comm = case_zc(rank, world)
     elif case == "zc_bidir_stream":
         comm = case_zc_bidir_stream(rank, world)
+    elif case == "host":
+        comm = case_host(rank, world)
     elif case == "zc_async":
         comm = case_zc_async(rank, world)
     elif case == "graph":

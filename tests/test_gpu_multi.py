@@ -62,6 +62,11 @@ def test_zero_copy_async_sends():
 
 
 @pytest.mark.parametrize("n", [2, 4])
+def test_step_with_host_buffers(n):
+    _run("host", n)
+
+
+@pytest.mark.parametrize("n", [2, 4])
 def test_step_cuda_graph(n):
     _run("graph", n)
 
