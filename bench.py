@@ -229,7 +229,7 @@ def main():
         args.graph = 0        # the CE engine's host-resolved slots are not graph-capturable
     if not args.chunk:
         # tuned on 2x B200 (profiles/r1_tune_step_ws.jsonl): 512 KiB chunks x 64 CTAs
-        # zero-copy pulls: 256 KiB grain; ring push: 512 KiB (profiles/r11_tune.jsonl)
+        # zero-copy pulls: 256 KiB grain; ring push: 512 KiB (profiles/r11_tune_zero_copy.jsonl)
         args.chunk = ((256 if args.zc else 512) << 10) if distributed else (128 << 10)
     S = args.pp
     nbytes = args.seq * args.hidden * 2

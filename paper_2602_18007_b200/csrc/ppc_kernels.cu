@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(kThreads) push_kernel(PushArgs a0) {
     cta_copy<false>(a.dst + off, a.src + off, len);
     // bar.sync orders every thread's stores before thread 0's release; the release
     // (fence.acq_rel + strong store, cumulative) publishes them to the peer.  One fence per
-    // CTA-chunk instead of one per thread (profiles/r1_probe: +6-15% at 32 MiB).
+    // CTA-chunk instead of one per thread (profiles/r1_nvlink_probe.md: +6-15% at 32 MiB).
     __syncthreads();
     if (threadIdx.x == 0) {
       fence_rel<kSys>();
