@@ -247,7 +247,52 @@ static int bidir() {
   return 0;
 }
 
+// Local HBM copy mode ("hbm", one GPU): the virtual-stage hand-off copy, SIMT vs TMA bulk.
+static int hbm() {
+  CK(cudaSetDevice(0));
+  const size_t maxb = 256ull << 20;
+  uint8_t *a, *b;
+  CK(cudaMalloc(&a, maxb)); CK(cudaMemset(a, 1, maxb));
+  CK(cudaMalloc(&b, maxb)); CK(cudaMemset(b, 0, maxb));
+  cudaStream_t st;
+  CK(cudaStreamCreate(&st));
+  const int S = 6;
+  for (int tile : {16 << 10, 32 << 10})
+    CK(cudaFuncSetAttribute(tma_copy<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, S * tile));
+  for (size_t bytes : {32ull << 20, 256ull << 20}) {
+    const int reps = bytes <= (32u << 20) ? 50 : 10;
+    auto run = [&](const char* name, int grid, auto launch) {
+      cudaEvent_t e0, e1;
+      CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
+      launch();
+      CK(cudaStreamSynchronize(st));
+      CK(cudaEventRecord(e0, st));
+      for (int r = 0; r < reps; ++r) launch();
+      CK(cudaEventRecord(e1, st));
+      CK(cudaEventSynchronize(e1));
+      CK(cudaGetLastError());
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      const double us = ms * 1e3 / reps;
+      printf("{\"hbm\": \"%s\", \"bytes\": %zu, \"grid\": %d, \"us\": %.2f, \"rw_gbps\": %.1f}\n",
+             name, bytes, grid, us, 2.0 * bytes / (us * 1e-6) / 1e9);
+      fflush(stdout);
+      cudaEventDestroy(e0); cudaEventDestroy(e1);
+    };
+    const size_t nv = bytes / 32;
+    for (int g : {148, 296, 592}) {
+      run("simt_u4", g, [&] { simt_copy<4, false><<<g, 512, 0, st>>>((V32*)b, (const V32*)a, nv); });
+      run("simt_u8", g, [&] { simt_copy<8, false><<<g, 512, 0, st>>>((V32*)b, (const V32*)a, nv); });
+      run("tma_32K", g, [&] { tma_copy<S><<<g, 32, S * (32 << 10), st>>>(b, a, bytes, 32 << 10); });
+      run("tma_16K", g, [&] { tma_copy<S><<<g, 32, S * (16 << 10), st>>>(b, a, bytes, 16 << 10); });
+    }
+    run("memcpy_d2d", 0, [&] { CK(cudaMemcpyAsync(b, a, bytes, cudaMemcpyDeviceToDevice, st)); });
+  }
+  return 0;
+}
+
 int main(int argc, char** argv) {
+  if (argc > 1 && std::string(argv[1]) == "hbm") return hbm();
   int n = 0;
   CK(cudaGetDeviceCount(&n));
   if (n < 2) { printf("{\"error\": \"needs 2 GPUs\"}\n"); return 0; }
