@@ -366,7 +366,10 @@ def main():
         peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
     achieved = alg / (avg_push_ms * 1e-3) / 1e9
     if not distributed:
-        kname, tkey = "ppc::copy_kernel (virtual-stage single-copy hand-off)", "copy_n1"
+        if os.environ.get("PPC_COPY_TMA_CTAS", "0") != "0":
+            kname, tkey = "ppc::copy_tma_kernel (virtual-stage TMA bulk hand-off)", "copy_tma_n1"
+        else:
+            kname, tkey = "ppc::copy_kernel (virtual-stage SIMT hand-off)", "copy_n1"
     elif zc_dom:
         kname = ("ppc::recv_kernel (zero-copy NVLink pull into the user buffer; CUDA events "
                  "on its stream, so the launch time includes the wait for the publication)")

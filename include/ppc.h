@@ -37,7 +37,10 @@
  *   PPC_ZC_STEPBUFS=1    the step driver's buffers (in the arena) are zero-copy sources
  *   PPC_LOCAL_DIRECT=1   virtual stages: single-copy hand-off instead of the ring
  *   PPC_LOCAL_QUEUE=0    virtual stages: serialise all copies of the GPU on one queue
- *   PPC_COPY_CTAS=296    virtual stages: CTAs of the hand-off copy kernel
+ *   PPC_COPY_CTAS=296    virtual stages: CTAs of the SIMT hand-off copy kernel
+ *   PPC_COPY_TMA_CTAS=0  virtual stages: >0 selects the TMA bulk hand-off copy with that
+ *                        many CTAs (16-B aligned buffers); 0 = the SIMT copy kernel
+ *                        (faster inside the overlapped step, profiles/r56_copy_engine_ab.jsonl)
  *   PPC_RECV_CTAS, PPC_STAGE_CTAS, PPC_PUSH_WS=1   grid / kernel-variant overrides
  */
 #ifndef PPC_H_

@@ -172,6 +172,7 @@ cudaError_t preload_kernels();
 // launch transport kernels with programmatic dependent launch (ppc_kernels.cu); set from
 // PPC_PDL by ppc_create
 extern int g_pdl;
+extern int g_copy_tma_ctas;
 // wait until *credit >= target (+ *seq_base when seq_base != nullptr: graph replay)
 cudaError_t launch_wait_credit(const uint64_t* credit, uint64_t target, ErrWord* err,
                                uint64_t timeout_ns, cudaStream_t s,

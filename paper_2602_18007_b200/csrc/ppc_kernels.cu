@@ -20,6 +20,7 @@
 namespace ppc {
 
 int g_pdl = 1;   // programmatic dependent launch for transport kernels (PPC_PDL, ppc_create)
+int g_copy_tma_ctas = 0;   // virtual-stage copy: TMA bulk grid; 0 = SIMT copy_kernel (PPC_COPY_TMA_CTAS)
 
 // Programmatic dependent launch (PDL): a transport kernel launched right behind another one
 // on the same stream may be scheduled while its predecessor still runs.  griddepcontrol.wait
@@ -783,9 +784,98 @@ __global__ void __launch_bounds__(kThreads, 2) copy_kernel(uint8_t* dst, const u
   for (uint64_t k = nv * sizeof(V32) + t; k < bytes; k += stride) dst[k] = src[k];
 }
 
+// K11 (TMA engine): the same copy through shared memory with bulk async copies
+// (cp.async.bulk global->shared completing on an mbarrier, shared->global in bulk groups).
+// One elected thread per CTA drives a kTmaStages-deep ring of kTmaTile-byte tiles; each CTA
+// owns a contiguous range of tiles.  Tile i+kTmaStages-1 is loaded into the stage tile i-1
+// used once that tile's store has finished reading shared memory (wait_group.read 1), so the
+// newest store and kTmaStages-1 loads stay in flight.  Needs 16-B aligned dst/src (bulk
+// copies move 16-B multiples); the last (bytes % 16) bytes are copied by thread 0 of the
+// last CTA.  Measured alone (tools/nvlink_probe hbm, profiles/r55_hbm_copy_probe.jsonl):
+// 8.3 us per 32 MiB vs 9.1 us for the SIMT copy at 148 CTAs; ncu in the step 11.1 vs
+// 11.8 us.  Inside the N=1 step, where F and B copies overlap, the SIMT copy is faster
+// (188.5 vs 190.9-193.9 us per step, profiles/r56_copy_engine_ab.jsonl), so it stays the
+// default and this engine is opt-in (PPC_COPY_TMA_CTAS > 0).
+constexpr int kTmaStages = 6;
+constexpr uint32_t kTmaTile = 16u << 10;
+constexpr uint32_t kTmaSmem = kTmaStages * kTmaTile;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void tma_ld(void* sdst, const void* gsrc, uint32_t n, uint64_t* mbar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+               ::"r"(smem_addr(mbar)), "r"(n) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_addr(sdst)), "l"(gsrc), "r"(n), "r"(smem_addr(mbar)) : "memory");
+}
+__device__ __forceinline__ void tma_st(void* gdst, const void* ssrc, uint32_t n) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+               ::"l"(gdst), "r"(smem_addr(ssrc)), "r"(n) : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* mbar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_addr(mbar)), "r"(phase) : "memory");
+}
+
+__global__ void __launch_bounds__(32) copy_tma_kernel(uint8_t* dst, const uint8_t* src,
+                                                      uint64_t bytes) {
+  extern __shared__ __align__(128) uint8_t tiles[];
+  __shared__ __align__(8) uint64_t mbar[kTmaStages];
+  pdl_enter();
+  if (threadIdx.x != 0) return;
+  const uint64_t body = bytes & ~15ull;
+  if (blockIdx.x == gridDim.x - 1)
+    for (uint64_t k = body; k < bytes; ++k) dst[k] = src[k];
+  const uint64_t ntiles = (body + kTmaTile - 1) / kTmaTile;
+  const uint64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
+  const uint64_t t0 = (uint64_t)blockIdx.x * per, t1 = min(ntiles, t0 + per);
+  if (t0 >= t1) return;
+  const uint64_t n = t1 - t0;
+  auto len = [&](uint64_t t) { return (uint32_t)min((uint64_t)kTmaTile, body - t * kTmaTile); };
+  for (int k = 0; k < kTmaStages; ++k)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&mbar[k])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  for (uint64_t j = 0; j < n && j < (uint64_t)kTmaStages; ++j)
+    tma_ld(tiles + j * kTmaTile, src + (t0 + j) * kTmaTile, len(t0 + j), &mbar[j]);
+  for (uint64_t i = 0; i < n; ++i) {
+    const int st = (int)(i % kTmaStages);
+    mbar_wait_parity(&mbar[st], (uint32_t)((i / kTmaStages) & 1));
+    tma_st(dst + (t0 + i) * kTmaTile, tiles + st * kTmaTile, len(t0 + i));
+    const uint64_t j = i - 1 + kTmaStages;   // refill the stage tile i-1 used
+    if (i >= 1 && j < n) {
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      const int sj = (int)((i - 1) % kTmaStages);
+      tma_ld(tiles + sj * kTmaTile, src + (t0 + j) * kTmaTile, len(t0 + j), &mbar[sj]);
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+
 cudaError_t launch_copy(void* dst, const void* src, uint64_t bytes, uint64_t chunk, int grid,
                         cudaStream_t s) {
   if (bytes == 0) return cudaSuccess;
+  if (g_copy_tma_ctas > 0 && bytes >= 16 && (((uintptr_t)dst | (uintptr_t)src) & 15) == 0) {
+    const uint64_t ntiles = ((bytes & ~15ull) + kTmaTile - 1) / kTmaTile;
+    const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(g_copy_tma_ctas, ntiles));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(g);
+    cfg.blockDim = dim3(32);
+    cfg.dynamicSmemBytes = kTmaSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = g_pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, copy_tma_kernel, static_cast<uint8_t*>(dst),
+                              static_cast<const uint8_t*>(src), bytes);
+  }
   return launch_k(copy_kernel, grid, kThreads, s, true, static_cast<uint8_t*>(dst),
                   static_cast<const uint8_t*>(src), bytes, chunk);
 }
@@ -846,7 +936,8 @@ cudaError_t preload_kernels() {
     const cudaError_t e = cudaFuncGetAttributes(&fa, f);
     if (e != cudaSuccess) return e;
   }
-  return cudaSuccess;
+  return cudaFuncSetAttribute(copy_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)kTmaSmem);
 }
 
 // ---------------------------------------------------------------- K14: test kernels

@@ -180,6 +180,31 @@ def test_xor_1f1b_step_matches_oracle(S, M, engine, direct, monkeypatch):
         c.destroy()
 
 
+@pytest.mark.parametrize("tma_ctas", [148, 7, 0])
+@pytest.mark.parametrize("n", [5, 16, 4096 + 3, 3 * (64 << 10) + 1234, (5 << 20) + 7])
+def test_direct_copy_engines(n, tma_ctas, monkeypatch):
+    """The virtual-stage hand-off copy (K11) in both engines: TMA bulk (148 CTAs, and 7 so
+    every CTA walks many tiles around its 6-stage ring) and SIMT (0, the default); sizes below one 16-B
+    bulk unit, exactly one, a partial tile, several tiles with a ragged tail, and more
+    tiles than CTAs.  Output bit-exact against the oracle's 1F1B simulation."""
+    monkeypatch.setenv("PPC_LOCAL_DIRECT", "1")
+    monkeypatch.setenv("PPC_COPY_TMA_CTAS", str(tma_ctas))
+    S, M = 3, 4
+    comms, Y, DX = _xor_step(S, M, n)
+    mask = _masks(n)
+    Yo, DXo, _, _ = run_1f1b(S, M, 2, xor_stage(mask, 0), xor_stage(mask, 1),
+                             lambda m: P.source_activation(42, 0, m, n),
+                             lambda m: P.source_gradient(42, 0, m, n), n, n, n)
+    for m in range(M):
+        assert np.array_equal(_host(Y[m])[:n], Yo[m]), m
+        assert np.array_equal(_host(DX[m])[:n], DXo[m]), m
+    for c in comms:
+        assert c.poll() == 0
+        c.disconnect()
+    for c in comms:
+        c.destroy()
+
+
 @pytest.mark.parametrize("direct", [1, 0])
 @pytest.mark.parametrize("fn", [True, False])
 @pytest.mark.parametrize("S", [2, 3])
