@@ -127,6 +127,23 @@ def ncu_traffic(key):
         return None
 
 
+def pcie_roofline(world, h2d_gpu, d2h_gpu, ms_step):
+    """The e2e step's host-link bound: each GPU's H2D and D2H bytes at the pinned-copy rates
+    measured with both directions busy and `world` GPUs copying at once
+    (profiles/pcie_roofline.json); null when that GPU count was not measured."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "pcie_roofline.json")) as fh:
+            r = json.load(fh)["both_dirs_gbps"].get(str(world))
+    except Exception:
+        r = None
+    if not r:
+        return None
+    bound_ms = max(h2d_gpu / (r["h2d"] * 1e6), d2h_gpu / (r["d2h"] * 1e6))
+    return {"bound": "pcie+host", "bound_ms_per_step": bound_ms, "frac": bound_ms / ms_step,
+            "h2d_gbps": r["h2d"], "d2h_gbps": r["d2h"],
+            "source": "profiles/pcie_roofline.json (tools/nvlink_probe pcie, r58)"}
+
+
 # ---------------------------------------------------------------- CPU oracle legs
 def oracle_step_sample(M_sample, nbytes, seed=42):
     """One bounded sample of the workload on the CPU oracle: a PP=2 1F1B step over M_sample
@@ -451,7 +468,8 @@ def main():
             if (hY and 0 in X) else None
         e2e = {"value": pipelines * M * args.seq * K2 / (ms_e2e * 1e-3), "unit": "tokens/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "ms_per_step": ms_e2e / K2, "steps": K2, "outputs_checked": ok}
+               "ms_per_step": ms_e2e / K2, "steps": K2, "outputs_checked": ok,
+               "roofline": pcie_roofline(world, h2d / world, d2h / world, ms_e2e / K2)}
         for c in comms:
             c.kernel_times(0), c.kernel_times(1)
 

@@ -8,6 +8,8 @@
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o nvlink_probe nvlink_probe.cu
 #include <cstdio>
 #include <cstdint>
+#include <cstring>
+#include <algorithm>
 #include <cstdlib>
 #include <string>
 #include <vector>
@@ -291,8 +293,52 @@ static int hbm() {
   return 0;
 }
 
+// PCIe mode ("pcie", one GPU): the e2e roofline.  Pinned host <-> device copies of 32 MiB
+// messages (the C2 boundary), 16 back to back per direction, H2D alone, D2H alone, and both
+// at once on two streams (the e2e step moves 512 MiB each way per step).
+static int pcie() {
+  CK(cudaSetDevice(0));
+  const size_t msg = 32ull << 20;
+  const int n = 16;
+  uint8_t *hin, *hout, *din, *dout;
+  CK(cudaMallocHost(&hin, msg * n)); memset(hin, 1, msg * n);
+  CK(cudaMallocHost(&hout, msg * n)); memset(hout, 0, msg * n);
+  CK(cudaMalloc(&din, msg * n));
+  CK(cudaMalloc(&dout, msg * n)); CK(cudaMemset(dout, 2, msg * n));
+  cudaStream_t sh, sd;
+  CK(cudaStreamCreateWithFlags(&sh, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking));
+  cudaEvent_t e0, e1, e2;
+  CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1)); CK(cudaEventCreate(&e2));
+  for (int mode = 0; mode < 3; ++mode)
+    for (int rep = 0; rep < 4; ++rep) {
+      CK(cudaDeviceSynchronize());
+      CK(cudaEventRecord(e0, sh));
+      CK(cudaStreamWaitEvent(sd, e0, 0));
+      for (int i = 0; i < n; ++i) {
+        if (mode != 1) CK(cudaMemcpyAsync(din + i * msg, hin + i * msg, msg, cudaMemcpyHostToDevice, sh));
+        if (mode != 0) CK(cudaMemcpyAsync(hout + i * msg, dout + i * msg, msg, cudaMemcpyDeviceToHost, sd));
+      }
+      CK(cudaEventRecord(e1, sh));
+      CK(cudaEventRecord(e2, sd));
+      CK(cudaDeviceSynchronize());
+      float a = 0, b = 0;
+      CK(cudaEventElapsedTime(&a, e0, e1));
+      CK(cudaEventElapsedTime(&b, e0, e2));
+      const float ms = mode == 0 ? a : mode == 1 ? b : std::max(a, b);
+      const double gb = (double)msg * n / 1e9;
+      printf("{\"pcie\": \"%s\", \"rep\": %d, \"bytes_per_dir\": %zu, \"ms\": %.3f, "
+             "\"h2d_gbps\": %.1f, \"d2h_gbps\": %.1f}\n",
+             mode == 0 ? "h2d" : mode == 1 ? "d2h" : "both", rep, msg * n, ms,
+             mode != 1 ? gb / (a * 1e-3) : 0.0, mode != 0 ? gb / (b * 1e-3) : 0.0);
+      fflush(stdout);
+    }
+  return 0;
+}
+
 int main(int argc, char** argv) {
   if (argc > 1 && std::string(argv[1]) == "hbm") return hbm();
+  if (argc > 1 && std::string(argv[1]) == "pcie") return pcie();
   int n = 0;
   CK(cudaGetDeviceCount(&n));
   if (n < 2) { printf("{\"error\": \"needs 2 GPUs\"}\n"); return 0; }
