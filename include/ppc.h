@@ -188,6 +188,35 @@ ppc_status_t ppc_pp_recv(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t bytes,
  * in the receiver's user buffer.  Used to time transfers end to end from the sender. */
 ppc_status_t ppc_pp_wait_consumed(ppc_comm_t* c, ppc_dir_t d, cudaStream_t s);
 
+/* Produce-in-place send: the stage's producing kernel writes the message straight into the
+ * receiver's ring slot over NVLink, so no separate send pass reads it back from HBM (the
+ * compute step fused with the transfer; P:L53's device-direct path without its staging
+ * copies).  ppc_pp_send_begin enqueues on s the slot's credit wait (bounded; a timeout
+ * latches PPC_ERR_TIMEOUT) and the 64-B header, and returns in *slot where to write:
+ *   payload   the receiver's slot (peer memory, a device pointer valid on the caller's GPU;
+ *             write [0, bytes) only, from kernels enqueued on s after this call)
+ *   flags     n_chunks per-chunk flags in the receiver's memory; chunk i covers
+ *             [i*chunk_bytes, min((i+1)*chunk_bytes, bytes))
+ *   seq       the value that marks a chunk complete
+ * A producer that signals itself stores chunk i, then (one thread, after a CTA barrier)
+ * fence.acq_rel.sys + st.release.sys flags[i] = seq — the receiver copies chunk i out as
+ * soon as its flag lands.  ppc_pp_send_end(flags_released = 0) enqueues one kernel that
+ * releases every flag after the producer's kernels (stream order); flags_released = 1
+ * means the producer released all of them.  One begin/end pair open per direction;
+ * bytes == 0 or > max_msg_bytes, a second begin, or an end without begin fail synchronously
+ * (PPC_ERR_INVALID_ARG / PPC_ERR_TOO_LARGE / PPC_ERR_STATE).  Not capturable into a step
+ * graph (the slot address depends on the sequence number): PPC_ERR_INVALID_ARG. */
+typedef struct {
+  void* payload;
+  unsigned long long* flags;
+  unsigned long long seq;
+  size_t bytes, chunk_bytes;
+  unsigned int n_chunks;
+} ppc_slot_t;
+ppc_status_t ppc_pp_send_begin(ppc_comm_t* c, ppc_dir_t d, size_t bytes, long long mb,
+                               cudaStream_t s, ppc_slot_t* slot);
+ppc_status_t ppc_pp_send_end(ppc_comm_t* c, ppc_dir_t d, int flags_released, cudaStream_t s);
+
 /* Zero-copy send buffers.  ppc_register(c, ptr, bytes) registers the device allocation that
  * contains [ptr, ptr+bytes) (one CUDA IPC handle per allocation) and returns a blob of
  * PPC_REG_BLOB_BYTES; the caller gives every PP neighbour the blob (control plane, e.g. a
@@ -292,6 +321,12 @@ ppc_status_t ppc_fill_payload(void* buf, size_t bytes, int seed, int step, int b
 typedef struct { int seed, step, stage, dir; } ppc_xor_ctx_t;
 int ppc_stage_xor(void* user, int mb, const void* in, void* out, size_t in_bytes,
                   size_t out_bytes, cudaStream_t s);
+/* The XOR stage proxy fused with its send (the produce-in-place pattern above): computes
+ * out = in XOR stream(ctx, mb) exactly as ppc_stage_xor and stores it straight into
+ * slot->payload, releasing each chunk's flag as soon as that chunk is written (call
+ * ppc_pp_send_end with flags_released = 1 afterwards).  bytes must equal slot->bytes. */
+ppc_status_t ppc_stage_xor_send(const ppc_slot_t* slot, const ppc_xor_ctx_t* ctx, int mb,
+                                const void* in, size_t bytes, cudaStream_t s);
 
 #ifdef __cplusplus
 }

@@ -72,6 +72,12 @@ class Step(C.Structure):
                 ("y", C.c_void_p), ("dx", C.c_void_p)]
 
 
+class Slot(C.Structure):
+    """ppc_slot_t: where a produce-in-place send writes (ppc_pp_send_begin)."""
+    _fields_ = [("payload", C.c_void_p), ("flags", C.c_void_p), ("seq", C.c_ulonglong),
+                ("bytes", C.c_size_t), ("chunk_bytes", C.c_size_t), ("n_chunks", C.c_uint)]
+
+
 class XorCtx(C.Structure):
     _fields_ = [("seed", C.c_int), ("step", C.c_int), ("stage", C.c_int), ("dir", C.c_int)]
 
@@ -92,6 +98,10 @@ _group = _sig("ppc_group", _i, [_vp, _i, C.POINTER(_i), C.POINTER(_i), C.POINTER
 _send = _sig("ppc_pp_send", _i, [_vp, _i, _vp, _sz, _ll, _vp])
 _recv = _sig("ppc_pp_recv", _i, [_vp, _i, _vp, _sz, _ll, _vp])
 _waitc = _sig("ppc_pp_wait_consumed", _i, [_vp, _i, _vp])
+_send_begin = _sig("ppc_pp_send_begin", _i, [_vp, _i, _sz, _ll, _vp, C.POINTER(Slot)])
+_send_end = _sig("ppc_pp_send_end", _i, [_vp, _i, _i, _vp])
+_xor_send = _sig("ppc_stage_xor_send", _i, [C.POINTER(Slot), C.POINTER(XorCtx), _i, _vp, _sz,
+                                             _vp])
 _sched = _sig("ppc_schedule_1f1b", _i, [_i, _i, _i, C.POINTER(Op), C.POINTER(_i)])
 _step = _sig("ppc_step_1f1b", _i, [_vp, C.POINTER(Step), _vp])
 _step_local = _sig("ppc_step_1f1b_local", _i, [C.POINTER(_vp), _i, C.POINTER(Step), C.POINTER(_vp)])
@@ -223,6 +233,25 @@ class Comm:
 
     def recv(self, *a, **k):
         _check(self.pp_recv(*a, **k), "ppc_pp_recv")
+
+    def send_begin(self, direction, nbytes, mb=0, stream=None) -> Slot:
+        """Produce-in-place send: returns the receiver's slot to write (ppc_pp_send_begin)."""
+        sl = Slot()
+        _check(_send_begin(self.h, direction, nbytes, mb, _stream(stream), C.byref(sl)),
+               "ppc_pp_send_begin")
+        return sl
+
+    def send_end(self, direction, flags_released=False, stream=None):
+        _check(_send_end(self.h, direction, int(bool(flags_released)), _stream(stream)),
+               "ppc_pp_send_end")
+
+    def xor_send(self, direction, ctx, mb, inp, nbytes, stream=None):
+        """The XOR stage proxy fused with its send: begin, ppc_stage_xor_send, end."""
+        sl = self.send_begin(direction, nbytes, mb, stream)
+        p = _ptr(inp)[0] if inp is not None else None
+        _check(_xor_send(C.byref(sl), C.byref(ctx), mb, p, nbytes, _stream(stream)),
+               "ppc_stage_xor_send")
+        self.send_end(direction, True, stream)
 
     def wait_consumed(self, direction, stream=None):
         _check(_waitc(self.h, direction, _stream(stream)), "ppc_pp_wait_consumed")

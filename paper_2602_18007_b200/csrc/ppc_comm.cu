@@ -456,7 +456,7 @@ ppc_status_t ppc_impl_zc_prepare(ppc_comm_t* c, ppc_dir_t d, const void* buf, si
   Chan& h = c->ch[d];
   if (h.peer_out < 0) return PPC_ERR_NO_NEIGHBOR;
   if (bytes > c->cfg.max_msg_bytes) return PPC_ERR_TOO_LARGE;
-  if (c->device < 0 || c->local_mode) return PPC_ERR_STATE;
+  if (c->device < 0 || c->local_mode || h.open_seq) return PPC_ERR_STATE;
   uint64_t zc_off = 0;
   const int zc_seg = find_reg(c, buf, bytes, &zc_off);
   if (zc_seg == -1) return PPC_ERR_INVALID_ARG;
@@ -483,7 +483,7 @@ ppc_status_t ppc_impl_send_ex(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_
   Chan& h = c->ch[d];
   if (h.peer_out < 0) return PPC_ERR_NO_NEIGHBOR;
   if (bytes > c->cfg.max_msg_bytes) return PPC_ERR_TOO_LARGE;
-  if (c->device < 0) return PPC_ERR_STATE;
+  if (c->device < 0 || h.open_seq) return PPC_ERR_STATE;
   DeviceGuard g(c->device);
   const uint64_t seq = h.send_seq + 1;
   const int slot = (int)(seq % c->K);
@@ -585,6 +585,81 @@ ppc_status_t ppc_impl_send_ex(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_
   // zero-copy: the send completes when the receiver has pulled it (on s_wait)
   if (ppc_status_t ts = time_mark(c, 0, zc_seg >= 0 ? s_wait : s, false)) return ts;
   h.send_seq = seq;
+  if (c->local_mode) CK(cudaEventRecord(h.sent_ev[slot], s));
+  return PPC_OK;
+}
+
+// Produce-in-place send (ppc.h): the CE engine's signalling (credit + header kernel before,
+// flags kernel after) around the caller's producer kernels instead of a copy.
+ppc_status_t ppc_pp_send_begin(ppc_comm_t* c, ppc_dir_t d, size_t bytes, long long mb,
+                               cudaStream_t s, ppc_slot_t* out) {
+  ppc_status_t st = check_live(c);
+  if (st) return st;
+  if (d != PPC_FWD && d != PPC_BWD) return PPC_ERR_INVALID_ARG;
+  if (mb < 0 || bytes == 0 || !out) return PPC_ERR_INVALID_ARG;
+  Chan& h = c->ch[d];
+  if (h.peer_out < 0) return PPC_ERR_NO_NEIGHBOR;
+  if (bytes > c->cfg.max_msg_bytes) return PPC_ERR_TOO_LARGE;
+  if (c->device < 0 || h.open_seq) return PPC_ERR_STATE;
+  if (c->capturing) return PPC_ERR_INVALID_ARG;
+  DeviceGuard g(c->device);
+  const uint64_t seq = h.send_seq + 1;
+  const int slot = (int)(seq % c->K);
+  uint64_t need = seq > (uint64_t)c->K ? seq - c->K : 0;
+  if (c->local_mode) {
+    if (need) {
+      Chan& rh = h.out_comm->ch[d];
+      if (rh.recv_seq < need) return PPC_ERR_WOULD_BLOCK;
+      CK(cudaStreamWaitEvent(s, rh.recvd_ev[slot], 0));
+    }
+    need = 0;
+  }
+  const uint32_t n_chunks = (uint32_t)((bytes + c->chunk - 1) / c->chunk);
+  CeHeadArgs a{};
+  a.hdr = h.o_hdr + slot;
+  a.hdr_flag = h.o_hdr_flag + slot;
+  a.credit = h.credit;
+  a.need_credit = need;
+  a.bytes = bytes;
+  a.seq = seq;
+  a.step = 0;
+  a.mb = mb;
+  a.dir = d;
+  a.boundary = (uint32_t)(d == PPC_FWD ? c->pp_i : c->pp_i - 1);
+  a.err = c->err_dev;
+  a.timeout_ns = c->timeout_ns;
+  a.rec = next_record(c);
+  a.rec_src = c->rank;
+  a.rec_dst = h.peer_out;
+  CK(launch_ce_head(a, s, true));
+  out->payload = h.o_payload + (size_t)slot * c->lay.stride;
+  out->flags = reinterpret_cast<unsigned long long*>(
+      h.o_flags + (size_t)slot * std::max<uint32_t>(c->lay.max_chunks, 1));
+  out->seq = seq;
+  out->bytes = bytes;
+  out->chunk_bytes = c->chunk;
+  out->n_chunks = n_chunks;
+  h.open_seq = seq;
+  h.open_chunks = n_chunks;
+  h.open_rec = a.rec;
+  return PPC_OK;
+}
+
+ppc_status_t ppc_pp_send_end(ppc_comm_t* c, ppc_dir_t d, int flags_released, cudaStream_t s) {
+  ppc_status_t st = check_live(c);
+  if (st) return st;
+  if (d != PPC_FWD && d != PPC_BWD) return PPC_ERR_INVALID_ARG;
+  Chan& h = c->ch[d];
+  if (!h.open_seq) return PPC_ERR_STATE;
+  DeviceGuard g(c->device);
+  const uint64_t seq = h.open_seq;
+  const int slot = (int)(seq % c->K);
+  uint64_t* flags = h.o_flags + (size_t)slot * std::max<uint32_t>(c->lay.max_chunks, 1);
+  if (!flags_released || h.open_rec)       // flags, or just the trace end stamp
+    CK(launch_ce_flags(flags, 0, flags_released ? 0 : h.open_chunks, seq, h.open_rec, s, true));
+  h.send_seq = seq;
+  h.open_seq = 0;
+  h.open_rec = nullptr;
   if (c->local_mode) CK(cudaEventRecord(h.sent_ev[slot], s));
   return PPC_OK;
 }

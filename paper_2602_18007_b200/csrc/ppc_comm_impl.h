@@ -82,6 +82,9 @@ struct Chan {
   uint64_t* credit = nullptr;        // ours; the receiver writes it
   uint32_t* push_done = nullptr;
   uint64_t send_seq = 0;
+  uint64_t open_seq = 0;             // ppc_pp_send_begin .. _end in progress (0 = none)
+  uint32_t open_chunks = 0;
+  ppc_record_t* open_rec = nullptr;
   ppc_comm* out_comm = nullptr;      // same-process peer
   // receiving side of direction d (peer_in -> we)
   int peer_in = -1;

@@ -181,8 +181,8 @@ cudaError_t launch_wait_credit(const uint64_t* credit, uint64_t target, ErrWord*
 cudaError_t launch_set_seq(uint64_t* seq, uint64_t v0, uint64_t v1, uint64_t v2, uint64_t v3,
                            cudaStream_t s);
 cudaError_t launch_recv(const RecvArgs& a, int grid, bool sys, cudaStream_t s);
-cudaError_t launch_ce_head(const CeHeadArgs& a, cudaStream_t s);
+cudaError_t launch_ce_head(const CeHeadArgs& a, cudaStream_t s, bool pdl = false);
 cudaError_t launch_ce_flags(uint64_t* flags, uint32_t c0, uint32_t c1, uint64_t seq,
-                            ppc_record_t* rec, cudaStream_t s);
+                            ppc_record_t* rec, cudaStream_t s, bool pdl = false);
 
 }  // namespace ppc

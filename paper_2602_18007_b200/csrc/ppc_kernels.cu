@@ -677,6 +677,7 @@ cudaError_t launch_publish(const PublishArgs& a, cudaStream_t s) {
 
 // ---------------------------------------------------------------- K12: CE signalling
 __global__ void ce_head_kernel(CeHeadArgs a) {
+  pdl_enter();
   const uint64_t t0 = globaltimer();
   if (a.rec) fill_record(a.rec, (long long)t0, a.rec_src, a.rec_dst, a.dir, 0, a.seq, a.mb, a.bytes);
   if (a.need_credit && !wait_geq(a.credit, a.need_credit, t0 + a.timeout_ns)) {
@@ -701,6 +702,7 @@ __global__ void ce_head_kernel(CeHeadArgs a) {
 // Runs after the copy engine finished this channel's bytes (stream order).
 __global__ void ce_flags_kernel(uint64_t* flags, uint32_t c0, uint32_t c1, uint64_t seq,
                                 ppc_record_t* rec) {
+  pdl_enter();
   fence_acq_rel_sys();
   for (uint32_t c = c0 + threadIdx.x; c < c1; c += blockDim.x) st_release_sys(flags + c, seq);
   if (rec && threadIdx.x == 0) rec->t_end_ns = (long long)globaltimer();
@@ -902,14 +904,12 @@ cudaError_t launch_recv(const RecvArgs& a, int grid, bool sys, cudaStream_t s) {
   grid = fit_grid(k, grid, kThreads);
   return launch_k(k, grid, kThreads, s, pdl_fits(k, grid, kThreads), a);
 }
-cudaError_t launch_ce_head(const CeHeadArgs& a, cudaStream_t s) {
-  ce_head_kernel<<<1, 1, 0, s>>>(a);
-  return cudaGetLastError();
+cudaError_t launch_ce_head(const CeHeadArgs& a, cudaStream_t s, bool pdl) {
+  return launch_k(ce_head_kernel, 1, 1, s, pdl, a);
 }
 cudaError_t launch_ce_flags(uint64_t* flags, uint32_t c0, uint32_t c1, uint64_t seq,
-                            ppc_record_t* rec, cudaStream_t s) {
-  ce_flags_kernel<<<1, 32, 0, s>>>(flags, c0, c1, seq, rec);
-  return cudaGetLastError();
+                            ppc_record_t* rec, cudaStream_t s, bool pdl) {
+  return launch_k(ce_flags_kernel, 1, 32, s, pdl, flags, c0, c1, seq, rec);
 }
 
 // Force-load every transport kernel on the current device.  With lazy module loading
@@ -918,6 +918,10 @@ cudaError_t launch_ce_flags(uint64_t* flags, uint32_t c0, uint32_t c1, uint64_t 
 // spinning on a peer would then block the peer's first receive launch until the wait
 // times out.  Touching the functions up front (cudaFuncGetAttributes loads them) keeps
 // every later launch free of module loads.
+__global__ void __launch_bounds__(kThreads) xor_send_kernel(uint8_t* out, uint64_t* flags,
+                                                            uint64_t seq, const uint8_t* in,
+                                                            uint64_t bytes, uint64_t chunk,
+                                                            uint32_t n_chunks, uint64_t key);
 cudaError_t preload_kernels() {
   cudaFuncAttributes fa;
   const void* fns[] = {
@@ -930,7 +934,7 @@ cudaError_t preload_kernels() {
       (const void*)wait_credit_kernel,     (const void*)set_seq_kernel,
       (const void*)add_kernel<float>,      (const void*)add_kernel<__half>,
       (const void*)add_kernel<__nv_bfloat16>, (const void*)add_kernel<int32_t>,
-      (const void*)copy_kernel,
+      (const void*)copy_kernel,            (const void*)xor_send_kernel,
   };
   for (const void* f : fns) {
     const cudaError_t e = cudaFuncGetAttributes(&fa, f);
@@ -986,7 +990,68 @@ __global__ void splitmix_xor_kernel(uint8_t* out, const uint8_t* in, uint64_t by
   }
 }
 
+// The XOR stage proxy fused with its send (ppc_stage_xor_send): CTA-per-chunk, the stage's
+// output goes straight into the receiver's slot (NVLink stores, 16 B per thread), then one
+// thread per CTA fences and releases that chunk's flag (the push kernel's protocol), so
+// the receiver copies chunk c out while later chunks are still being produced.
+__global__ void __launch_bounds__(kThreads) xor_send_kernel(uint8_t* out, uint64_t* flags,
+                                                            uint64_t seq, const uint8_t* in,
+                                                            uint64_t bytes, uint64_t chunk,
+                                                            uint32_t n_chunks, uint64_t key) {
+  pdl_enter();                     // the slot's credit wait (ce_head_kernel) has completed
+  const uint64_t base = mix64(key + kGamma);
+  const bool vec = ((((uintptr_t)out) | ((uintptr_t)in)) & 15) == 0 && (chunk & 15) == 0;
+  for (uint32_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+    const uint64_t off = (uint64_t)c * chunk, end = min(off + chunk, bytes);
+    uint64_t k = off;
+    if (vec) {                     // word pairs (w, w+1), w even, inside the chunk
+      const uint64_t np = (end - off) / 16;
+      for (uint64_t p = threadIdx.x; p < np; p += blockDim.x) {
+        const uint64_t w = off / 8 + 2 * p;
+        uint64_t v0 = mix64(base + (w + 1) * kGamma), v1 = mix64(base + (w + 2) * kGamma);
+        if (in) {
+          const uint4 x = ld_src(reinterpret_cast<const uint4*>(in + 8 * w));
+          v0 ^= (uint64_t)x.x | (uint64_t)x.y << 32;
+          v1 ^= (uint64_t)x.z | (uint64_t)x.w << 32;
+        }
+        uint4 y;
+        y.x = (uint32_t)v0; y.y = (uint32_t)(v0 >> 32);
+        y.z = (uint32_t)v1; y.w = (uint32_t)(v1 >> 32);
+        st_data(reinterpret_cast<uint4*>(out + 8 * w), y);
+      }
+      k = off + np * 16;
+    }
+    for (uint64_t b = k + threadIdx.x; b < end; b += blockDim.x) {   // bytewise remainder
+      const uint64_t v = mix64(base + (b / 8 + 1) * kGamma);
+      uint8_t x = (uint8_t)(v >> (8 * (b & 7)));
+      if (in) x ^= in[b];
+      out[b] = x;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      fence_acq_rel_sys();
+      st_release_sys(flags + c, seq);
+    }
+  }
+}
+
 }  // namespace ppc
+
+extern "C" ppc_status_t ppc_stage_xor_send(const ppc_slot_t* slot, const ppc_xor_ctx_t* ctx,
+                                           int mb, const void* in, size_t bytes,
+                                           cudaStream_t s) {
+  if (!slot || !ctx || !slot->payload || !slot->flags || bytes == 0 || bytes != slot->bytes ||
+      slot->chunk_bytes == 0 || slot->n_chunks != (bytes + slot->chunk_bytes - 1) / slot->chunk_bytes)
+    return PPC_ERR_INVALID_ARG;
+  const int grid = (int)std::min<uint32_t>(slot->n_chunks, 128u);
+  const cudaError_t e = ppc::launch_k(
+      ppc::xor_send_kernel, grid, ppc::kThreads, s, true, static_cast<uint8_t*>(slot->payload),
+      reinterpret_cast<uint64_t*>(slot->flags), (uint64_t)slot->seq,
+      static_cast<const uint8_t*>(in), (uint64_t)bytes, (uint64_t)slot->chunk_bytes,
+      (uint32_t)slot->n_chunks,
+      ppc::payload_key(ctx->seed ^ 0x8000, ctx->step, ctx->stage, ctx->dir, mb));
+  return e == cudaSuccess ? PPC_OK : PPC_ERR_CUDA;
+}
 
 extern "C" ppc_status_t ppc_fill_payload(void* buf, size_t bytes, int seed, int step,
                                          int boundary, int dir, long long mb, cudaStream_t s) {

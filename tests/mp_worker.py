@@ -486,6 +486,52 @@ def case_hetero(rank, world):
     return comm
 
 
+def case_inplace(rank, world, M=6):
+    """Produce-in-place sends along a PP=world chain, both directions: every stage computes
+    the XOR proxy of what it received straight into the next stage's ring slot — even mb
+    with the fused kernel (per-chunk flags from the producer, ppc_stage_xor_send), odd mb
+    with ppc_stage_xor writing into the slot and ppc_pp_send_end releasing the flags."""
+    import ctypes as C
+    S, n = world, 5 * (256 << 10) + 777
+    cfg = ppc.make_config(pp=S, max_msg_bytes=n, chunk_bytes=256 << 10)
+    comm = ppc.connect_distributed(cfg, rank, world, rank, with_nccl=False)
+    s = torch.cuda.current_stream()
+    xor = ppc._lib.ppc_stage_xor
+    xor.restype = C.c_int
+    xor.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t,
+                    C.c_void_p]
+    mask = lambda st, d, m: P.proxy_mask(42, 0, st, d, m, n)
+
+    def forward(d, m, inp):
+        ctx = ppc.XorCtx(42, 0, rank, d)
+        if m % 2 == 0:
+            comm.xor_send(d, ctx, m, inp, n, stream=s)
+        else:
+            sl = comm.send_begin(d, n, m, stream=s)
+            assert xor(C.byref(ctx), m, inp.data_ptr(), sl.payload, n, n, s.cuda_stream) == 0
+            comm.send_end(d, False, stream=s)
+
+    for m in range(M):
+        for d in (ppc.FWD, ppc.BWD):
+            first = 0 if d == ppc.FWD else S - 1
+            last = S - 1 if d == ppc.FWD else 0
+            x = buf(n)
+            if rank == first:
+                ppc.fill_payload(x, n, 42, 0, 0, d, m, stream=s)
+            else:
+                comm.recv(d, x, n, mb=m, stream=s)
+            if rank != last:
+                forward(d, m, x)
+            else:
+                want = P.payload_bytes(42, 0, 0, d, m, n)
+                for st in (range(S - 1) if d == ppc.FWD else range(S - 1, 0, -1)):
+                    want = want ^ mask(st, d, m)
+                assert np.array_equal(host(x)[:n], want), (rank, d, m)
+    torch.cuda.synchronize()
+    assert comm.poll() == 0
+    return comm
+
+
 def main():
     case = sys.argv[1]
     rank = int(os.environ["RANK"])
@@ -526,6 +572,8 @@ def main():
         comm = case_zc_async(rank, world)
     elif case == "graph":
         comm = case_graph(rank, world)
+    elif case == "inplace":
+        comm = case_inplace(rank, world)
     elif case == "fullsize":
         comm = case_fullsize(rank, world)
     elif case == "gather":

@@ -2,6 +2,7 @@
 process (the intra-device ring, K11), through the C-ABI.  Every comparison is element by
 element against the oracle (oracle/transfer.py, oracle/proxy.py) on the same seeded
 inputs (synth/payload.py), bit-exact."""
+import ctypes as C
 import hashlib
 
 import numpy as np
@@ -52,6 +53,52 @@ def test_send_recv_bit_exact(K, sizes):
             comms[snd].send(d, src, n, mb=i, stream=s)
             comms[rcv].recv(d, dst, n, mb=i, stream=s)
             assert np.array_equal(_host(dst)[:n], P.payload_bytes(42, 0, 0, d, i, n)), (i, n, d)
+    for c in comms:
+        assert c.poll() == 0
+        c.disconnect()
+    for c in comms:
+        c.destroy()
+
+
+@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("n", [5, 4096 + 3, 3 * (64 << 10) + 1234])
+@pytest.mark.parametrize("K", [1, 2])
+def test_produce_in_place_send(K, n, fused):
+    """ppc_pp_send_begin / _end: the producer writes straight into the receiver's ring slot.
+    fused: the XOR stage proxy releases each chunk's flag itself (ppc_stage_xor_send);
+    otherwise a plain producer (the payload fill, written into the slot) and send_end
+    releases the flags.  Both directions, more messages than slots, bit-exact vs the
+    oracle's payload / mask streams."""
+    comms = _pair(max_msg_bytes=n, ring_slots=K, chunk_bytes=64 << 10)
+    s = torch.cuda.current_stream()
+    for m in range(4):
+        for d, (snd, rcv) in ((ppc.FWD, (0, 1)), (ppc.BWD, (1, 0))):
+            dst = _buf(n)
+            dst.fill_(0xAB)
+            want = P.payload_bytes(42, 0, 0, d, m, n)
+            if fused:
+                src = _buf(n)
+                ppc.fill_payload(src, n, 42, 0, 0, d, m, stream=s)
+                comms[snd].xor_send(d, ppc.XorCtx(42, 0, snd, d), m, src, n, stream=s)
+                want = want ^ P.proxy_mask(42, 0, snd, d, m, n)
+            else:
+                sl = comms[snd].send_begin(d, n, m, stream=s)
+                assert sl.bytes == n and sl.seq == m + 1
+                ppc.fill_payload(sl.payload, n, 42, 0, 0, d, m, stream=s)
+                comms[snd].send_end(d, False, stream=s)
+            comms[rcv].recv(d, dst, n, mb=m, stream=s)
+            assert np.array_equal(_host(dst)[:n], want), (m, d)
+    # state errors: second begin, a plain send while a slot is open, end without begin
+    sl = comms[0].send_begin(ppc.FWD, n, 4, stream=s)
+    st = ppc.STATUS.index("STATE")
+    assert ppc._send_begin(comms[0].h, ppc.FWD, n, 5, None, C.byref(ppc.Slot())) == st
+    assert comms[0].pp_send(ppc.FWD, _buf(n), n, 5, s) == st
+    assert ppc._send_end(comms[0].h, ppc.BWD, 0, None) == st
+    ppc.fill_payload(sl.payload, n, 42, 0, 0, 0, 4, stream=s)
+    comms[0].send_end(ppc.FWD, False, stream=s)
+    dst = _buf(n)
+    comms[1].recv(ppc.FWD, dst, n, mb=4, stream=s)
+    assert np.array_equal(_host(dst)[:n], P.payload_bytes(42, 0, 0, 0, 4, n))
     for c in comms:
         assert c.poll() == 0
         c.disconnect()

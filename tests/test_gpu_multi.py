@@ -31,6 +31,11 @@ def test_two_gpus(case):
     _run(case, 2)
 
 
+@pytest.mark.parametrize("n", [2, 4])
+def test_produce_in_place_chain(n):
+    _run("inplace", n)
+
+
 @pytest.mark.parametrize("case", ["xor_sm", "xor_ce", "xor_pull"])
 def test_four_gpu_pipeline(case):
     _run(case, 4)
