@@ -42,7 +42,11 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--engine", default="sm")
     ap.add_argument("--out", default="gpurun_out/exposure.jsonl")
+    ap.add_argument("--inplace", action="store_true",
+                    help="PPC_STEP_INPLACE=1: stage fns produce straight into the peer's slot")
     a = ap.parse_args()
+    if a.inplace:
+        os.environ["PPC_STEP_INPLACE"] = "1"
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(rank)
     dist.init_process_group("gloo")
@@ -56,11 +60,13 @@ def main():
     def compute(inp, out, reps, stream):
         with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
             h = x0 if inp is None else inp.view(T, H)
-            for _ in range(reps):
+            for r in range(reps):
                 for l in range(a.layers):
-                    h = torch.nn.functional.silu(h @ W1[l]) @ W2[l]
-            if out is not None:
-                out.view(T, H).copy_(h)
+                    last = out is not None and r == reps - 1 and l == a.layers - 1
+                    # the last GEMM's epilogue stores straight into `out` (with
+                    # PPC_STEP_INPLACE: the receiver's ring slot, over NVLink)
+                    h = torch.matmul(torch.nn.functional.silu(h @ W1[l]), W2[l],
+                                     out=out.view(T, H) if last else None)
 
     def fwd(user, mb, inp, out, ib, ob, stream):
         compute(as_bf16(inp, T * H) if inp and ib else None, as_bf16(out, T * H) if out and ob else None,
@@ -94,6 +100,7 @@ def main():
     assert comm.poll() == 0
     if rank == 0:
         rec = {"pp": S, "M": M, "layers_per_stage": a.layers, "engine": a.engine,
+               "produce_in_place": a.inplace,
                "ms_step": res["full"], "ms_step_flags_only": res["flags_only"],
                "exposed_frac": (res["full"] - res["flags_only"]) / res["full"],
                "tokens_per_s": M * T / (res["full"] * 1e-3),

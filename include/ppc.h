@@ -35,6 +35,10 @@
  *   PPC_ZC_SIDE=0        step driver: publish zero-copy sends on the send stream instead
  *                        of the compute stream
  *   PPC_ZC_STEPBUFS=1    the step driver's buffers (in the arena) are zero-copy sources
+ *   PPC_STEP_INPLACE=0   step driver: a stage fn whose output is sent writes it straight
+ *                        into the receiver's ring slot (ppc_pp_send_begin / _end) instead
+ *                        of a local buffer that a send then moves (not in graph capture
+ *                        or the virtual-stage direct mode)
  *   PPC_LOCAL_DIRECT=1   virtual stages: single-copy hand-off instead of the ring
  *   PPC_LOCAL_QUEUE=0    virtual stages: serialise all copies of the GPU on one queue
  *   PPC_COPY_CTAS=296    virtual stages: CTAs of the SIMT hand-off copy kernel

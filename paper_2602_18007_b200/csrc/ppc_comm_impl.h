@@ -154,6 +154,7 @@ struct ppc_comm {
   std::vector<int> members[3];
   cudaStream_t side[2] = {nullptr, nullptr};   // send streams of the step driver
   cudaStream_t zcw[2] = {nullptr, nullptr};    // step driver: zero-copy consumption waits
+  bool step_inplace = false;                   // step driver: stage fns produce into the slot
   bool zc_side = false;                        // step driver publishes zero-copy on side[d]
   bool fuse_publish = true;                    // step driver: publish from the prior receive
   bool zc_stepbufs = true;                     // step driver buffers are zero-copy sources

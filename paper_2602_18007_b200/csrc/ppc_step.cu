@@ -111,6 +111,7 @@ struct Stepper {
   Mailbox* inbox[2] = {nullptr, nullptr};
   Mailbox* outbox[2] = {nullptr, nullptr};
   bool fused_next = false;      // the next op's send was fused into this op's receive
+  bool inplace_sent = false;    // this op's stage fn produced straight into the peer's slot
   bool used_ds = false;         // a terminal output went to host memory through sb.ds
   bool dmode = false;
   cudaStream_t xq = nullptr;    // direct mode: the GPU's transfer queue (nullptr: own stream)
@@ -309,7 +310,19 @@ struct Stepper {
       if (phase == 1) {                                  // stage compute
         ppc_stage_fn fn = kind == 0 ? st->fwd : st->bwd;
         void* user = kind == 0 ? st->fwd_user : st->bwd_user;
-        if (has_out) {
+        if (has_out && fn && bytes && c->step_inplace && !dmode && !c->capturing) {
+          // produce in place: the stage fn writes the boundary tensor straight into the
+          // receiver's ring slot (ppc_pp_send_begin / _end on the compute stream), so no
+          // send pass re-reads it from HBM
+          ppc_slot_t sl;
+          ppc_status_t bs = ppc_pp_send_begin(c, (ppc_dir_t)d, bytes, m, cs, &sl);
+          if (bs == PPC_ERR_WOULD_BLOCK) return PPC_OK;
+          if (bs) return bs;
+          if (fn(user, m, in, sl.payload, in ? bytes : 0, bytes, cs) != 0) return PPC_ERR_INVALID_ARG;
+          mark_read(in, d, bi);
+          if (ppc_status_t es = ppc_pp_send_end(c, (ppc_dir_t)d, 0, cs)) return es;
+          inplace_sent = true;
+        } else if (has_out) {
           if (fn || !in) {
             if (dmode) {
               ppc_status_t e = PPC_OK;
@@ -380,6 +393,8 @@ struct Stepper {
       if (phase == 2) {                                  // send
         if (has_out && fused_next) {
           fused_next = false;                            // already published (fusion)
+        } else if (has_out && inplace_sent) {
+          inplace_sent = false;                          // produced into the slot
         } else if (has_out) {
           if (dmode) {
             // hand the buffer to the next stage: it makes the one copy

@@ -572,6 +572,9 @@ def main():
         comm = case_zc_async(rank, world)
     elif case == "graph":
         comm = case_graph(rank, world)
+    elif case == "xor_inplace":           # the step's stage fns produce into the slot
+        os.environ["PPC_STEP_INPLACE"] = "1"
+        comm = case_xor(rank, world, ppc.ENGINE_SM)
     elif case == "inplace":
         comm = case_inplace(rank, world)
     elif case == "fullsize":

@@ -252,6 +252,31 @@ def test_direct_copy_engines(n, tma_ctas, monkeypatch):
         c.destroy()
 
 
+@pytest.mark.parametrize("K", [1, 2])
+@pytest.mark.parametrize("S,M", [(2, 1), (2, 4), (3, 4), (4, 8)])
+def test_xor_step_produce_in_place(S, M, K, monkeypatch):
+    """PPC_STEP_INPLACE=1: in the 1F1B step every stage fn whose output is sent writes it
+    straight into the receiver's ring slot (ppc_pp_send_begin / _end on the compute stream;
+    the sender blocks on a full ring as in the oracle's event model, A4).  Virtual stages,
+    ring path; outputs bit-exact vs the oracle's 1F1B simulation."""
+    monkeypatch.setenv("PPC_LOCAL_DIRECT", "0")
+    monkeypatch.setenv("PPC_STEP_INPLACE", "1")
+    n = 3 * (64 << 10) + 1234
+    comms, Y, DX = _xor_step(S, M, n, K=K)
+    mask = _masks(n)
+    Yo, DXo, _, _ = run_1f1b(S, M, K, xor_stage(mask, 0), xor_stage(mask, 1),
+                             lambda m: P.source_activation(42, 0, m, n),
+                             lambda m: P.source_gradient(42, 0, m, n), n, n, n)
+    for m in range(M):
+        assert np.array_equal(_host(Y[m])[:n], Yo[m]), m
+        assert np.array_equal(_host(DX[m])[:n], DXo[m]), m
+    for c in comms:
+        assert c.poll() == 0
+        c.disconnect()
+    for c in comms:
+        c.destroy()
+
+
 @pytest.mark.parametrize("direct", [1, 0])
 @pytest.mark.parametrize("fn", [True, False])
 @pytest.mark.parametrize("S", [2, 3])

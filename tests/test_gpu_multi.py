@@ -36,6 +36,11 @@ def test_produce_in_place_chain(n):
     _run("inplace", n)
 
 
+@pytest.mark.parametrize("n", [2, 4])
+def test_step_produce_in_place(n):
+    _run("xor_inplace", n)
+
+
 @pytest.mark.parametrize("case", ["xor_sm", "xor_ce", "xor_pull"])
 def test_four_gpu_pipeline(case):
     _run(case, 4)
