@@ -312,7 +312,7 @@ ppc_status_t ppc_disconnect(ppc_comm_t* c);        /* phase 1: close peer handle
 ppc_status_t ppc_destroy(ppc_comm_t* c);           /* phase 2 (after a caller barrier)     */
 const char* ppc_status_str(ppc_status_t st);
 /* sizeof of the ABI structs, for bindings to check their layouts: which = 0 ppc_config_t,
- * 1 ppc_step_t, 2 ppc_record_t, 3 ppc_op_t; 0 for any other value. */
+ * 1 ppc_step_t, 2 ppc_record_t, 3 ppc_op_t, 4 ppc_slot_t; 0 for any other value. */
 size_t ppc_struct_size(int which);
 
 /* ---- test/bench kernels (K14); not part of the transfer path --------------------------- */

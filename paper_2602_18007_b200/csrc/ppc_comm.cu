@@ -93,6 +93,7 @@ size_t ppc_struct_size(int which) {
     case 1: return sizeof(ppc_step_t);
     case 2: return sizeof(ppc_record_t);
     case 3: return sizeof(ppc_op_t);
+    case 4: return sizeof(ppc_slot_t);
   }
   return 0;
 }

@@ -33,7 +33,7 @@ def test_struct_layouts_match_the_binding():
     lib = ctypes.CDLL(ppc.lib_path())
     lib.ppc_struct_size.restype = ctypes.c_size_t
     lib.ppc_struct_size.argtypes = [ctypes.c_int]
-    for which, cls in enumerate([ppc.Config, ppc.Step, ppc.Record, ppc.Op]):
+    for which, cls in enumerate([ppc.Config, ppc.Step, ppc.Record, ppc.Op, ppc.Slot]):
         assert lib.ppc_struct_size(which) == ctypes.sizeof(cls), cls.__name__
     assert lib.ppc_struct_size(7) == 0
 
@@ -96,6 +96,17 @@ def test_host_only_data_path_is_state_error():
     assert comms[0].pp_send(ppc.FWD, 0, 16, 0) == ppc.STATUS.index("INVALID_ARG")  # null buf
     assert comms[0].pp_send(ppc.FWD, 0x1000, 16, -1) == ppc.STATUS.index("INVALID_ARG")
     assert comms[0].pp_send(ppc.FWD, 0x1000, 16, 0) == ppc.STATUS.index("STATE")  # no device
+    # produce-in-place send: argument / state errors are synchronous and host-only
+    sl = ctypes.byref(ppc.Slot())
+    begin, end = ppc._send_begin, ppc._send_end
+    assert begin(comms[0].h, ppc.BWD, 16, 0, None, sl) == ppc.STATUS.index("NO_NEIGHBOR")
+    assert begin(comms[0].h, ppc.FWD, 0, 0, None, sl) == ppc.STATUS.index("INVALID_ARG")
+    assert begin(comms[0].h, ppc.FWD, 16, -1, None, sl) == ppc.STATUS.index("INVALID_ARG")
+    assert begin(comms[0].h, ppc.FWD, 16, 0, None, None) == ppc.STATUS.index("INVALID_ARG")
+    assert begin(comms[0].h, ppc.FWD, 64 << 20, 0, None, sl) == ppc.STATUS.index("TOO_LARGE")
+    assert begin(comms[0].h, ppc.FWD, 16, 0, None, sl) == ppc.STATUS.index("STATE")  # no device
+    assert end(comms[0].h, ppc.FWD, 0, None) == ppc.STATUS.index("STATE")     # nothing open
+    assert end(comms[0].h, 7, 0, None) == ppc.STATUS.index("INVALID_ARG")
     for c in comms:
         c.destroy()
 
