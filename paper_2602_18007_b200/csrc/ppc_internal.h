@@ -110,6 +110,7 @@ struct RecvArgs {
   uint32_t has_pub;
   PublishArgs pub;
 };
+extern int g_recv_early;
 cudaError_t launch_publish(const PublishArgs& a, cudaStream_t s);
 
 // TP-sliced receive with a fused all-gather (ppc_pp_recv_gather).

@@ -20,6 +20,7 @@
 namespace ppc {
 
 int g_pdl = 1;   // programmatic dependent launch for transport kernels (PPC_PDL, ppc_create)
+int g_recv_early = 0;   // receive looks for its publication before griddepcontrol.wait (PPC_RECV_EARLY)
 int g_copy_tma_ctas = 0;   // virtual-stage copy: TMA bulk grid; 0 = SIMT copy_kernel (PPC_COPY_TMA_CTAS)
 
 // Programmatic dependent launch (PDL): a transport kernel launched right behind another one
@@ -522,14 +523,67 @@ __device__ __forceinline__ void fused_publish_flag(const PublishArgs* p0, uint64
 // kPub: the variant with the fused publication (step driver, terminal receives of a
 // comm-only PP2 step); it needs 88 registers (one CTA per SM), so the plain variant, which
 // shares SMs with the push kernels of deeper pipelines, is kept at 64.
-template <bool kSys, bool kPub>
+// mapped base of a zero-copy source segment on this GPU; 0 if never imported
+__device__ __forceinline__ uint64_t zc_base(const RecvArgs& a, uint32_t seg) {
+  return seg == kArenaSeg ? (uint64_t)(uintptr_t)a.peer_arena
+       : (a.seg_tab && seg < (uint32_t)kMaxSeg) ? a.seg_tab[seg] : 0;
+}
+constexpr int kEarlyV = 4;                    // V32 vectors per thread pulled early (64 KiB/CTA)
+
+template <bool kSys, bool kPub, bool kEarly = false>
 __global__ void __launch_bounds__(kThreads) recv_kernel(const __grid_constant__ RecvArgs a0) {
+  __shared__ const uint8_t* s_zc_src;   // zero-copy: the sender's buffer, mapped here
+  __shared__ const uint8_t* s_early_src;
+  __shared__ uint64_t s_early_seq;
+  // Early phase (kEarly: PPC_RECV_EARLY, PDL only; its own instantiation, the early
+  // registers would halve the occupancy of the plain kernel): before griddepcontrol.wait, ONE look (no spin) at this
+  // message's header.  If its zero-copy publication is already there, the CTA pulls the
+  // first 64 KiB of its first chunk into registers while the predecessor drains.  Only
+  // peer-published data is read here; nothing is written.  The graph's sequence base may
+  // still be stale (set_seq_kernel is a predecessor), so after the wait the early result is
+  // used only if the resolved seq is the same.
+  V32 pre[kEarlyV];
+  bool pre_ok = false;
+  if (kEarly) {
+    if (threadIdx.x == 0) {
+      s_early_src = nullptr;
+      const RecvArgs e = resolve(a0);
+      if ((int64_t)(ld_acq<kSys>(e.hdr_flag) - e.seq) >= 0) {
+        const volatile SlotHeader* h = e.hdr;
+        if (h->magic == kMagic && h->seq == e.seq && h->mb == e.mb && h->bytes == e.bytes &&
+            (h->flags & kHdrZeroCopy)) {
+          const uint64_t base = zc_base(e, h->src_seg);
+          if (base) {
+            s_early_src = reinterpret_cast<const uint8_t*>(base + h->src_off);
+            s_early_seq = e.seq;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    const uint64_t off = (uint64_t)blockIdx.x * a0.chunk;
+    if (s_early_src && blockIdx.x < a0.n_chunks &&
+        min(a0.chunk, a0.bytes - off) >= (uint64_t)kEarlyV * kThreads * sizeof(V32) &&
+        (((uintptr_t)(a0.dst + off) | (uintptr_t)(s_early_src + off)) & 31) == 0) {
+      const V32* src = reinterpret_cast<const V32*>(s_early_src + off);
+#pragma unroll
+      for (int j = 0; j < kEarlyV; ++j) pre[j] = ld_src(src + threadIdx.x + j * kThreads);
+      pre_ok = true;
+    }
+  }
   pdl_enter();
   const RecvArgs a = resolve(a0);
-  __shared__ const uint8_t* s_zc_src;   // zero-copy: the sender's buffer, mapped here
   uint64_t deadline = 0;
   int fail = 0;
-  if (threadIdx.x == 0) {
+  if (kEarly && threadIdx.x == 0 && s_early_src && s_early_seq == a.seq) {
+    // header already checked in the early phase (same seq, so the same slot and message)
+    s_zc_src = s_early_src;
+    if (a.rec && blockIdx.x == 0) {
+      fill_record(a.rec, (long long)globaltimer(), a.rec_src, a.rec_dst, -1, 1, a.seq, a.mb, a.bytes);
+      a.rec->t_start_ns = (long long)globaltimer();
+    }
+    if (kPub && blockIdx.x == 0 && !fused_publish_header(&a0.pub)) fail = 1;
+  } else if (threadIdx.x == 0) {
     const uint64_t t0 = globaltimer();
     deadline = t0 + a.timeout_ns;
     s_zc_src = nullptr;
@@ -553,8 +607,7 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(const __grid_constant__ 
         fail = 1;
       } else if (h->flags & kHdrZeroCopy) {
         const uint32_t seg = h->src_seg;
-        const uint64_t base = seg == kArenaSeg ? (uint64_t)(uintptr_t)a.peer_arena
-                            : (a.seg_tab && seg < (uint32_t)kMaxSeg) ? a.seg_tab[seg] : 0;
+        const uint64_t base = zc_base(a, seg);
         if (!base) {                   // the receiver never imported that registration
           latch(a.err, PPC_ERR_ORDER, a.seq, 0x300u | seg << 12);
           fail = 1;
@@ -568,11 +621,20 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(const __grid_constant__ 
   }
   if (__syncthreads_or(fail)) return;
   const uint8_t* zc_src = s_zc_src;
+  // the early pull is valid only for the message resolved now (CTA-uniform condition)
+  const bool use_pre = kEarly && pre_ok && zc_src == s_early_src && s_early_seq == a.seq;
   for (uint32_t c = blockIdx.x; c < a.n_chunks; c += gridDim.x) {
     const uint64_t off = (uint64_t)c * a.chunk;
     const uint64_t len = min(a.chunk, a.bytes - off);
     if (zc_src) {                      // payload complete at publication: pull it over NVLink
-      cta_copy<true>(a.dst + off, zc_src + off, len);
+      uint64_t skip = 0;
+      if (use_pre && c == blockIdx.x) {
+        V32* d = reinterpret_cast<V32*>(a.dst + off);
+#pragma unroll
+        for (int j = 0; j < kEarlyV; ++j) st_data(d + threadIdx.x + j * kThreads, pre[j]);
+        skip = (uint64_t)kEarlyV * kThreads * sizeof(V32);
+      }
+      cta_copy<true>(a.dst + off + skip, zc_src + off + skip, len - skip);
       continue;
     }
     int f = 0;
@@ -902,7 +964,12 @@ cudaError_t launch_recv(const RecvArgs& a, int grid, bool sys, cudaStream_t s) {
                      : (sys ? recv_kernel<true, false> : recv_kernel<false, false>);
   if (sys) grid = std::min(grid, kMaxSpinGrid);
   grid = fit_grid(k, grid, kThreads);
-  return launch_k(k, grid, kThreads, s, pdl_fits(k, grid, kThreads), a);
+  const bool pdl = pdl_fits(k, grid, kThreads);
+  if (sys && g_pdl && g_recv_early) {   // zero-copy pulls over NVLink; without PDL nothing runs early
+    auto ke = a.has_pub ? recv_kernel<true, true, true> : recv_kernel<true, false, true>;
+    if (pdl_fits(ke, grid, kThreads)) return launch_k(ke, grid, kThreads, s, true, a);
+  }
+  return launch_k(k, grid, kThreads, s, pdl, a);
 }
 cudaError_t launch_ce_head(const CeHeadArgs& a, cudaStream_t s, bool pdl) {
   return launch_k(ce_head_kernel, 1, 1, s, pdl, a);
@@ -928,6 +995,7 @@ cudaError_t preload_kernels() {
       (const void*)push_kernel<true>,      (const void*)push_kernel<false>,
       (const void*)push_ws_kernel<true>,   (const void*)push_ws_kernel<false>,
       (const void*)recv_kernel<true, false>, (const void*)recv_kernel<false, false>,
+      (const void*)recv_kernel<true, false, true>, (const void*)recv_kernel<true, true, true>,
       (const void*)recv_kernel<true, true>,  (const void*)recv_kernel<false, true>,
       (const void*)gather_kernel,          (const void*)publish_kernel,
       (const void*)ce_head_kernel,         (const void*)ce_flags_kernel,
