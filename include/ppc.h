@@ -30,6 +30,9 @@
  * Environment (read by ppc_create / the step driver; defaults are the measured best,
  * DESIGN.md §6-7):
  *   PPC_PDL=1            programmatic dependent launch of the transport kernels
+ *   PPC_RECV_EARLY=0     cross-GPU receives (with PDL) look once for their zero-copy
+ *                        publication before waiting on the predecessor kernel and pull the
+ *                        first 64 KiB of each CTA's first chunk into registers meanwhile
  *   PPC_FUSE_PUBLISH=1   step driver: a zero-copy source op's publication rides on the
  *                        preceding terminal receive kernel
  *   PPC_ZC_SIDE=0        step driver: publish zero-copy sends on the send stream instead
