@@ -13,14 +13,15 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 PORT = [29611]
 
 
-def _run(case, n, timeout=240):
+def _run(case, n, timeout=240, env=None):
     if torch.cuda.device_count() < n:
         pytest.skip(f"needs {n} GPUs")
     PORT[0] += 1
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(PORT[0]),
            os.path.join(HERE, "mp_worker.py"), case]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout,
+                       env=None if env is None else {**os.environ, **env})
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count(f"{case} OK") == n
 
@@ -65,6 +66,13 @@ def test_zero_copy_registered_pull(case):
 
 def test_zero_copy_bidirectional_stream():
     _run("zc_bidir_stream", 2)
+
+
+@pytest.mark.parametrize("case", ["zc", "zc_bidir_stream", "zc_async", "graph"])
+def test_zero_copy_early_receive(case):
+    """PPC_RECV_EARLY=1: receives look for their publication before griddepcontrol.wait
+    and pull their first 64 KiB early (a stale graph sequence base must be discarded)."""
+    _run(case, 2, env={"PPC_RECV_EARLY": "1"})
 
 
 def test_zero_copy_async_sends():
