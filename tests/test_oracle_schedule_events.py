@@ -206,3 +206,54 @@ def test_trace_csv_schema_and_order():
     assert len(rows) == 2 * 2 * 4
     keys = [(row[0], row[2]) for row in rows]
     assert keys == sorted(keys)
+
+
+# ---- max-min sharing of per-GPU egress / ingress (O2 "shared"; R6).
+# Hand-derived progressive-filling results; a filling that ignores the ingress constraint,
+# never releases capacity, or releases it from the wrong resource fails at least one.
+def _rates(flows, egress=1.0, ingress=1.0):
+    from oracle.events import Msg, _maxmin_rates
+    ms = [Msg(0, 0, a, b, i + 1, 0, 1, 0.0) for i, (a, b) in enumerate(flows)]
+    _maxmin_rates(ms, LinkModel(bw=1.0, mode="shared", egress=egress, ingress=ingress))
+    return [m.rate for m in ms]
+
+
+def test_maxmin_two_flows_share_one_egress():
+    # A->B, A->C: GPU A's egress (1) is the only shared resource -> 1/2 each
+    assert _rates([(0, 1), (0, 2)]) == pytest.approx([0.5, 0.5])
+
+
+def test_maxmin_ingress_binds():
+    # A->C, B->C share C's ingress -> 1/2 each; D->E alone -> 1 (an egress-only model
+    # would give all three 1)
+    assert _rates([(0, 2), (1, 2), (3, 4)]) == pytest.approx([0.5, 0.5, 1.0])
+
+
+def test_maxmin_three_flow_classic():
+    # A->B, A->C, D->C: A's egress and C's ingress both have 2 users (share 1/2); after
+    # freezing A's flows at 1/2, C's ingress has 1/2 left for D->C -> 1/2, 1/2, 1/2
+    assert _rates([(0, 1), (0, 2), (3, 2)]) == pytest.approx([0.5, 0.5, 0.5])
+
+
+def test_maxmin_capacity_released_from_the_right_resource():
+    # A->B, A->C, A->D, E->D: A's egress (3 users, 1/3) is tightest; D's ingress keeps
+    # 1 - 1/3 = 2/3 for E->D (not 1/2: the freed share must be subtracted from D's ingress)
+    assert _rates([(0, 1), (0, 2), (0, 3), (4, 3)]) == pytest.approx([1 / 3] * 3 + [2 / 3])
+
+
+def test_maxmin_unequal_caps():
+    # egress 1, ingress 0.6: a lone flow gets min(1, 0.6); two flows into one GPU 0.3 each
+    assert _rates([(0, 1)], ingress=0.6) == pytest.approx([0.6])
+    assert _rates([(0, 1), (2, 1)], ingress=0.6) == pytest.approx([0.3, 0.3])
+
+
+@pytest.mark.parametrize("mode,units", [("shared", 8), ("independent", 6)])
+def test_pp3_comm_only_makespan_hand_derived(mode, units):
+    """PP3, M = 3, zero compute, message time t (DESIGN.md §2 R6, worked out there step by
+    step): the middle stage's FWD (c2) and BWD (e0) sends overlap in [4t, 6t) and share its
+    egress, and stage 1's ingress is shared by a2 and d0 in [2t, 4t) -> T = 8t; with
+    independent links the same schedule takes 6t."""
+    nbytes, bw = 1 << 20, 1e5
+    r = simulate(3, 3, 0.0, 0.0, nbytes, nbytes, LinkModel(bw=bw, mode=mode), K=4)
+    validate_trace(r, 3)
+    assert r.makespan == pytest.approx(units * nbytes / bw, rel=1e-12)
