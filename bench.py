@@ -3,22 +3,30 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ppc|reference]
 
-Workload (BASELINE.json configs[1], "C2"): LLaMA-8B-shaped boundary [1,4096,4096] bf16
-(32 MiB per message), PP = 2, M = 8 micro-batches, non-interleaved 1F1B, comm-only step
-(identity stage functions, R13).  A step = every FWD and BWD send/recv of one
-1F1B step of every pipeline.
-  * N = 1: the two stages are virtual stages on one GPU (the intra-device ring, K11);
+Headline workload (BASELINE.json configs[1], "C2"): LLaMA-8B-shaped boundary [1,4096,4096]
+bf16 (32 MiB per message), PP = 2, M = 8 micro-batches, non-interleaved 1F1B, comm-only step
+(identity stage functions, R13).  A step = every FWD and BWD send/recv of one 1F1B
+step of every pipeline.
+  * N = 1: the two stages are virtual stages on one GPU: the single-copy hand-off (headline)
+    and, beside it, the intra-device ring (push into the ring slot + copy-out);
   * N >= 2: one process per GPU (torchrun), N/2 independent PP=2 pipelines (weak scaling,
-    no data-path collective), rings mapped over NVLink with CUDA IPC.
+    no data-path collective), rings and registered buffers mapped over NVLink (CUDA IPC).
 value = tokens/s of the whole job = pipelines * M * seq * K / T, T = max over ranks of the
-CUDA-event time of the K timed steps.
+CUDA-event time of the K timed steps.  Beside the headline, the same run measures: the
+BASELINE north-star configurations that fit the GPU count (N = 4: PP4 M16 (C3 per TP
+pipeline) and PP4 M32 Qwen (C4 stand-in); N = 8: C3 = PP4 x TP2 M16 with DCBS (NCCL TP
+groups) and C4 = PP8 M32 Qwen), the CPU-Forwarding baseline B1 (libppcb) on the same
+workload, the end-to-end path with host buffers, and the CPU oracle.
 """
 from __future__ import annotations
 
 import argparse
 import json
+import multiprocessing as mp
 import os
+import platform
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -29,17 +37,25 @@ sys.path.insert(0, ROOT)
 METRIC = "1F1B tokens/s (stage-boundary P2P, device-direct)"
 NVLINK_GBPS = 900.0          # NVLink 5 per direction per GPU (nominal; R4)
 
+# BASELINE.json configs (SURVEY §8 sizes): name -> (pp, tp, M, hidden, model)
+WORKLOADS = {
+    "C2": (2, 1, 8, 4096, "LLaMA-8B"),
+    "C3": (4, 2, 16, 4096, "LLaMA-8B"),
+    "C4": (8, 1, 32, 3584, "Qwen2-7B"),
+    "C3-pp4": (4, 1, 16, 4096, "LLaMA-8B"),      # one TP pipeline of C3 (4-GPU stand-in)
+    "C4-pp4": (4, 1, 32, 3584, "Qwen2-7B"),      # C4 on 4 GPUs (stand-in)
+}
+EXTRA = {1: [], 2: [], 4: ["C3-pp4", "C4-pp4"], 8: ["C3", "C4"]}
 
-def parse():
+
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ppc", choices=["ppc", "reference"])
-    ap.add_argument("--pp", type=int, default=2)
-    ap.add_argument("--M", type=int, default=8)
+    ap.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))
     ap.add_argument("--seq", type=int, default=4096)
-    ap.add_argument("--hidden", type=int, default=4096)
     ap.add_argument("--engine", default="sm", choices=["sm", "ce", "pull"])
     ap.add_argument("--chunk", type=int, default=0,
                     help="flag / pull granularity; 0 = tuned default (256 KiB zero-copy, "
@@ -52,13 +68,56 @@ def parse():
     ap.add_argument("--zc", type=int, default=-1,
                     help="N>=2: register the step's source buffers (zero-copy NVLink pulls); "
                          "-1 = on for pp = 2 (every send is then a pull), off for deeper "
-                         "pipelines: a pull moves data only when the receiver reaches its "
-                         "receive, while a push runs ahead into the K-slot ring, which the "
-                         "warm-up of a deep 1F1B pipeline exploits (PP4 M16: 3623 us "
-                         "all-pull vs 2868 us, profiles/r38_pp4_zc_vs_ring.jsonl)")
+                         "pipelines (a push runs ahead into the K-slot ring, which the warm-up "
+                         "of a deep 1F1B pipeline exploits; profiles/r38_pp4_zc_vs_ring.jsonl)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    return ap.parse_args()
+    ap.add_argument("--no-b1", action="store_true", help="skip the CPU-Forwarding B1 arm")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the north-star configurations beside the headline")
+    ap.add_argument("--no-ring", action="store_true", help="N=1: skip the intra-device ring line")
+    return ap.parse_args(argv)
+
+
+# ---------------------------------------------------------------- workload resolution
+def resolve(args, world, name=None):
+    """The configuration one run of `name` uses at `world` ranks (both arms print it)."""
+    name = name or args.workload
+    pp, tp, M, hidden, model = WORKLOADS[name]
+    virtual = world == 1
+    if virtual and (pp != 2 or tp != 1):
+        raise SystemExit(f"{name} needs {pp * tp} GPUs")
+    if not virtual and world % (pp * tp):
+        raise SystemExit(f"--gpus {world} is not a multiple of pp*tp = {pp * tp}")
+    zc = args.zc if args.zc >= 0 else (1 if pp == 2 else 0)
+    zc = bool(zc) and not virtual
+    chunk = args.chunk or ((128 << 10) if virtual else ((256 << 10) if zc else (512 << 10)))
+    pipelines = 1 if virtual else world // pp
+    return {"name": name, "pp": pp, "tp": tp, "dp": 1 if virtual else world // (pp * tp),
+            "M": M, "seq": args.seq, "hidden": hidden, "model": model,
+            "msg_bytes": args.seq * hidden * 2, "virtual": virtual, "pipelines": pipelines,
+            "zc": zc, "chunk": chunk, "engine": args.engine, "channels": args.channels,
+            "cta": args.cta, "slots": args.slots or pp + 1,
+            "graph": bool(args.graph) and args.engine != "ce"}
+
+
+def config_dict(wl, world):
+    tag = f"{wl['name']}: " if wl["name"] in ("C2", "C3", "C4") else f"{wl['name']} (stand-in): "
+    layout = (f"PP={wl['pp']} x TP={wl['tp']} (DCBS: NCCL TP groups, custom-kernel PP)"
+              if wl["tp"] > 1 else f"PP={wl['pp']}")
+    where = ("two virtual stages on one GPU" if wl["virtual"] else
+             f"{wl['pipelines']} independent pipeline(s) on {world} GPUs")
+    per_dir = wl["M"] * wl["msg_bytes"]
+    return {"workload": f"{tag}{wl['model']}-shaped {layout} boundary [1,{wl['seq']},"
+                        f"{wl['hidden']}] bf16, M={wl['M']}, 1F1B comm-only step, {where}",
+            "pp": wl["pp"], "tp": wl["tp"], "pipelines": wl["pipelines"],
+            "virtual_stages": wl["virtual"], "M": wl["M"], "seq": wl["seq"],
+            "hidden": wl["hidden"], "msg_bytes": wl["msg_bytes"], "engine": wl["engine"],
+            "chunk_bytes": wl["chunk"], "channels": wl["channels"], "ring_slots": wl["slots"],
+            "zero_copy_sends": wl["zc"], "cuda_graph": wl["graph"],
+            "l2": (f"inputs larger than L2 (M x {wl['msg_bytes'] / 2**20:g} MiB per stage per "
+                   f"direction = {per_dir / 2**20:g} MiB > 126 MB)" if per_dir > 126e6 else
+                   "inputs fit in L2: latency run, not a bench line")}
 
 
 # ---------------------------------------------------------------- clocks (NVML, during timing)
@@ -85,7 +144,7 @@ class ClockSampler:
             "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
             "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
         }
-        while not self._stop.is_set():
+        while True:
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
@@ -94,6 +153,8 @@ class ClockSampler:
                         self.reasons.add(k)
             except Exception:
                 pass
+            if self._stop.is_set():
+                break
             time.sleep(0.001)
 
     def start(self):
@@ -119,7 +180,8 @@ def measured_peaks():
 
 
 def ncu_traffic(key):
-    """Per-launch dram read+write bytes of the dominant kernel from a committed ncu capture."""
+    """Per-launch traffic of the dominant kernel from a committed ncu capture
+    (profiles/ncu_traffic.json): local DRAM read+write bytes (N = 1) or NVLink bytes (N >= 2)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             return json.load(fh).get(key)
@@ -128,9 +190,7 @@ def ncu_traffic(key):
 
 
 def pcie_roofline(world, h2d_gpu, d2h_gpu, ms_step):
-    """The e2e step's host-link bound: each GPU's H2D and D2H bytes at the pinned-copy rates
-    measured with both directions busy and `world` GPUs copying at once
-    (profiles/pcie_roofline.json); null when that GPU count was not measured."""
+    """The e2e step's host-link bound (profiles/pcie_roofline.json); null if unmeasured."""
     try:
         with open(os.path.join(ROOT, "profiles", "pcie_roofline.json")) as fh:
             r = json.load(fh)["both_dirs_gbps"].get(str(world))
@@ -145,364 +205,612 @@ def pcie_roofline(world, h2d_gpu, d2h_gpu, ms_step):
 
 
 # ---------------------------------------------------------------- CPU oracle legs
-def oracle_step_sample(M_sample, nbytes, seed=42):
-    """One bounded sample of the workload on the CPU oracle: a PP=2 1F1B step over M_sample
-    micro-batches of the same boundary tensors (identity stages), byte-level transfers with
-    header checks and digests (oracle/proxy.py + oracle/transfer.py).  Returns seconds."""
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return platform.processor() or None
+
+
+def oracle_step(pp, M, nbytes, seed=42):
+    """One full 1F1B step of the workload on the CPU oracle (oracle/proxy.py + transfer.py):
+    PP stages, M micro-batches of `nbytes` messages each way, byte-level ring transfers with
+    header checks and digests, identity stages; outputs checked.  Returns seconds."""
     import numpy as np
     from oracle.proxy import run_1f1b
     from synth import payload as P
     t0 = time.perf_counter()
-    X = {m: P.source_activation(seed, 0, m, nbytes) for m in range(M_sample)}
-    G = {m: P.source_gradient(seed, 0, m, nbytes) for m in range(M_sample)}
+    X = {m: P.source_activation(seed, 0, m, nbytes) for m in range(M)}
+    G = {m: P.source_gradient(seed, 0, m, nbytes) for m in range(M)}
     ident = lambda s, m, x: x
-    Y, DX, chans, _ = run_1f1b(2, M_sample, 2, ident, ident, X.__getitem__, G.__getitem__,
-                               nbytes, nbytes, nbytes)
-    assert all(np.array_equal(Y[m], X[m]) for m in range(M_sample))
+    Y, DX, _, _ = run_1f1b(pp, M, pp + 1, ident, ident, X.__getitem__, G.__getitem__,
+                           nbytes, nbytes, nbytes)
+    assert all(np.array_equal(Y[m], X[m]) and np.array_equal(DX[m], G[m]) for m in range(M))
     return time.perf_counter() - t0
 
 
-def cpu_baseline(args, nbytes):
-    M_s = 2
-    secs = oracle_step_sample(M_s, nbytes)
-    reps = max(1, min(5, int(15.0 / max(secs, 1e-3))))
-    times = [secs] + [oracle_step_sample(M_s, nbytes) for _ in range(reps - 1)]
-    t = statistics.median(times)
-    return {"value": M_s * args.seq / t, "unit": "tokens/s", "cores": 1, "kind": "oracle",
-            "sample": f"PP=2 1F1B step over {M_s} of the {args.M} micro-batches "
-                      f"([1,{args.seq},{args.hidden}] bf16 = {nbytes} B messages), "
-                      f"byte-level ring transfer with header checks + blake2b digests, "
-                      f"median of {len(times)} runs, single thread"}
+def _oracle_worker(a):
+    return oracle_step(*a)
+
+
+def cpu_baseline(wl, budget_s=30.0):
+    """the oracle as it stands on this host's cores — one full step of the
+    headline workload single-process, then P concurrent full steps (one per process, P =
+    usable cores bounded by memory) for the all-core throughput."""
+    pp, M, nb = wl["pp"], wl["M"], wl["msg_bytes"]
+    tokens = wl["M"] * wl["seq"]
+    t1 = oracle_step(pp, M, nb)
+    cores = len(os.sched_getaffinity(0))
+    per_proc = 6 * M * nb                      # X, G, rings, outputs, digests (generous)
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 16 << 30
+    P = max(1, min(cores, int(0.5 * avail // per_proc)))
+    tall = None
+    if P > 1 and t1 * 1.5 < budget_s:
+        ctx = mp.get_context("fork")
+        t0 = time.perf_counter()
+        with ctx.Pool(P) as pool:
+            pool.map(_oracle_worker, [(pp, M, nb)] * P)
+        tall = time.perf_counter() - t0
+    moved = 2 * (pp - 1) * M * nb             # bytes the step transfers (both directions)
+    out = {"value": tokens / t1, "unit": "tokens/s", "cores": 1, "kind": "oracle",
+           "sample": f"one full {wl['name']} step (PP={pp}, M={M}, {2 * (pp - 1) * M} messages "
+                     f"of {nb} B, byte-level ring transfers + header checks + digests), "
+                     f"single process",
+           "gib_per_s": moved / t1 / 2**30, "s_per_step": t1, "cpu_model": cpu_model(),
+           "host_cores": cores}
+    if tall is not None:
+        out["all_cores"] = {"value": P * tokens / tall, "unit": "tokens/s", "cores": P,
+                            "processes": P, "s_wall": tall,
+                            "gib_per_s": P * moved / tall / 2**30,
+                            "sample": f"{P} concurrent full steps, one per process"}
+    return out
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle as the reference arm (rank 0 only)."""
+    """--impl reference: the CPU oracle as the reference arm (rank 0 only), timed on the
+    GPU arm's config: every step is one full oracle step of the headline workload."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    nbytes = args.seq * args.hidden * 2
-    M_s = 2
-    for _ in range(args.warmup):
-        oracle_step_sample(M_s, nbytes)
-    t = sum(oracle_step_sample(M_s, nbytes) for _ in range(args.steps))
-    value = M_s * args.seq * args.steps / t
+    world = args.gpus
+    wl = resolve(args, world)
+    tokens = wl["pipelines"] * wl["M"] * wl["seq"]
+    pp, M, nb = wl["pp"], wl["M"], wl["msg_bytes"]
+    # bounded: one full step of ONE pipeline per timed step (pipelines are independent and
+    # identical; the value scales by the pipeline count, as the GPU arm's does)
+    t_one = oracle_step(pp, M, nb)
+    steps, warm = args.steps, args.warmup
+    if (steps + warm) * t_one > 240:           # keep the whole run within a few minutes
+        steps, warm = max(1, int(200 / t_one)), 0
+    for _ in range(warm):
+        oracle_step(pp, M, nb)
+    t = sum(oracle_step(pp, M, nb) for _ in range(steps))
+    value = tokens * steps / t
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * t / steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": workload_config(args, pipelines=1, virtual=False),
+            "config": config_dict(wl, world),
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": 1, "kind": "oracle",
-                             "sample": f"PP=2 1F1B step over {M_s} micro-batches per step"},
+                             "sample": f"{steps} full {wl['name']} oracle steps (one pipeline "
+                                       f"each, x{wl['pipelines']} pipelines), single process",
+                             "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
+    if steps != args.steps:
+        line["steps_timed"] = steps
     print(json.dumps(line), flush=True)
 
 
-def workload_config(args, pipelines, virtual):
-    name = "C2: " if (args.pp, args.hidden, args.M) == (2, 4096, 8) else ""
-    model = "Qwen2-7B" if args.hidden == 3584 else "LLaMA-8B"
-    return {"workload": f"{name}{model}-shaped PP={args.pp} boundary [1,{args.seq},{args.hidden}] "
-                        f"bf16, M={args.M}, 1F1B comm-only step",
-            "pp": args.pp, "pipelines": pipelines, "virtual_stages": virtual, "M": args.M,
-            "seq": args.seq, "hidden": args.hidden, "msg_bytes": args.seq * args.hidden * 2,
-            "engine": args.engine, "chunk_bytes": args.chunk, "channels": args.channels,
-            "ring_slots": args.slots or args.pp + 1, "zero_copy_sends": bool(args.zc) and not virtual,
-            "cuda_graph": bool(args.graph),
-            "l2": l2_note(args)}
-
-
-def l2_note(args):
-    """How the timing rule on L2 is met: the per-stage working set of one step vs 126 MB L2."""
-    msg = args.seq * args.hidden * 2
-    per_dir = args.M * msg
-    if per_dir > 126 * 10**6:
-        return (f"inputs larger than L2 (M x {msg / 2**20:g} MiB per stage per direction, "
-                f"{per_dir / 2**20:g} MiB)")
-    return f"inputs fit in L2 ({per_dir} B per stage per direction): latency run, not a bench line"
-
-
 # ---------------------------------------------------------------- GPU arm
+class Ctx:
+    """Process-level state of the GPU arm."""
+
+    def __init__(self):
+        import torch
+        import torch.distributed as dist
+        import paper_2602_18007_b200 as ppc
+        self.torch, self.dist, self.ppc = torch, dist, ppc
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.distributed = self.world > 1
+        if self.distributed:
+            torch.cuda.set_device(self.local)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(0)
+        self.dev = torch.cuda.current_device()
+
+    def barrier(self):
+        self.torch.cuda.synchronize()
+        if self.distributed:
+            self.dist.barrier()
+
+    def max_over_ranks(self, v):
+        if not self.distributed:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(self, v):
+        if not self.distributed:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64)
+        self.dist.all_reduce(t)
+        return float(t.item())
+
+    def all_true(self, b):
+        return self.sum_over_ranks(0.0 if b else 1.0) == 0.0
+
+
+class Pipeline:
+    """This process's stages of one workload: comms, device buffers X / G / Y / DX, streams,
+    step args, optional CUDA graph."""
+
+    def __init__(self, ctx, wl, local_direct=True):
+        torch, ppc = ctx.torch, ctx.ppc
+        self.ctx, self.wl = ctx, wl
+        os.environ["PPC_LOCAL_DIRECT"] = "1" if local_direct else "0"
+        S, nb, M = wl["pp"], wl["msg_bytes"], wl["M"]
+        engine = {"sm": ppc.ENGINE_SM, "ce": ppc.ENGINE_CE, "pull": ppc.ENGINE_PULL}[wl["engine"]]
+        cfg = ppc.make_config(tp=wl["tp"], pp=S, dp=wl["dp"], max_msg_bytes=nb,
+                              ring_slots=wl["slots"], channels=wl["channels"],
+                              chunk_bytes=wl["chunk"], engine=engine,
+                              cta_per_channel=wl["cta"], trace=3)
+        if ctx.distributed:
+            self.comms = [ppc.connect_distributed(cfg, ctx.rank, ctx.world, ctx.local,
+                                                  with_nccl=wl["tp"] > 1)]
+            self.stages = [self.comms[0].group(ppc.GROUP_PP)[0].index(ctx.rank)]
+        else:
+            self.comms = ppc.virtual_stages(cfg, ctx.dev)
+            self.stages = list(range(S))
+        dev = ctx.dev
+        bufs = lambda: [torch.empty(nb, dtype=torch.uint8, device=dev) for _ in range(M)]
+        self.X = {s: bufs() for s in self.stages if s == 0}
+        self.G = {s: bufs() for s in self.stages if s == S - 1}
+        self.Y = {s: bufs() for s in self.stages if s == S - 1}
+        self.DX = {s: bufs() for s in self.stages if s == 0}
+        for s in self.stages:
+            for m in range(M):
+                if s in self.X:
+                    ppc.fill_payload(self.X[s][m], nb, 42, 0, 0xFF, 0, m)
+                if s in self.G:
+                    ppc.fill_payload(self.G[s][m], nb, 42, 0, 0xFF, 1, m)
+        self.args = [ppc.StepArgs(M, nb, nb, x=self.X.get(s), g=self.G.get(s),
+                                  y=self.Y.get(s), dx=self.DX.get(s)) for s in self.stages]
+        self.streams = [torch.cuda.Stream() for _ in self.stages]
+        if ctx.distributed and wl["zc"]:
+            ppc.register_tensors(self.comms[0], [t for s in self.stages
+                                                 for t in self.X.get(s, []) + self.G.get(s, [])])
+        self.graph = None
+        self.step(eager=True)              # allocates the step buffers
+        ctx.barrier()
+        if wl["graph"]:
+            self.graph = ppc.StepGraph(self.comms, self.args, self.streams)
+
+    def step(self, args=None, eager=False):
+        ppc = self.ctx.ppc
+        if self.graph is not None and args is None and not eager:
+            self.graph.launch()
+            return
+        a = args or self.args
+        if self.ctx.distributed:
+            ppc.step_1f1b(self.comms[0], a[0], self.streams[0])
+        else:
+            ppc.step_1f1b_local(self.comms, a, self.streams)
+
+    def timed(self, steps, instrumented=False):
+        """K steps between barriers + synchronize; CUDA events on the launch streams (the
+        graph replays on streams[0]); max over ranks.  Returns ms for the K steps."""
+        torch, ctx = self.ctx.torch, self.ctx
+        for c in self.comms:
+            c.set_trace(2 if instrumented else 0)
+            c.kernel_times(0), c.kernel_times(1)
+        sts = self.streams[:1] if (self.graph is not None and not instrumented) else self.streams
+        ev0 = [torch.cuda.Event(enable_timing=True) for _ in sts]
+        ev1 = [torch.cuda.Event(enable_timing=True) for _ in sts]
+        ctx.barrier()
+        for e, st in zip(ev0, sts):
+            e.record(st)
+        for _ in range(steps):
+            self.step(eager=instrumented)
+        for e, st in zip(ev1, sts):
+            e.record(st)
+        ctx.barrier()
+        return ctx.max_over_ranks(max(a.elapsed_time(b) for a, b in zip(ev0, ev1)))
+
+    def outputs_ok(self):
+        """Device-side check of every micro-batch after the timed steps: identity stages, so
+        the last stage must hold X_m and stage 0 G_m (compared with the pipeline's own
+        inputs on the ranks that have them; otherwise with a fresh SplitMix fill)."""
+        torch, ppc = self.ctx.torch, self.ctx.ppc
+        ok = True
+        nb = self.wl["msg_bytes"]
+        ref = torch.empty(nb, dtype=torch.uint8, device=self.ctx.dev)
+        for s in self.stages:
+            for m in range(self.wl["M"]):
+                if s in self.Y:
+                    ppc.fill_payload(ref, nb, 42, 0, 0xFF, 0, m)
+                    ok &= bool(torch.equal(self.Y[s][m], ref))
+                if s in self.DX:
+                    ppc.fill_payload(ref, nb, 42, 0, 0xFF, 1, m)
+                    ok &= bool(torch.equal(self.DX[s][m], ref))
+        return self.ctx.all_true(ok)
+
+    def close(self):
+        ctx = self.ctx
+        ctx.barrier()
+        if self.graph is not None:
+            self.graph.destroy()
+        for c in self.comms:
+            c.disconnect()
+        if ctx.distributed:
+            ctx.dist.barrier()
+        for c in self.comms:
+            c.destroy()
+        os.environ.pop("PPC_LOCAL_DIRECT", None)
+
+
+def measure(ctx, wl, steps, warmup, local_direct=True):
+    """Steady-state K-step timing of one workload; returns the summary and the pipeline."""
+    p = Pipeline(ctx, wl, local_direct)
+    for _ in range(warmup):
+        p.step()
+    ctx.barrier()
+    ms = p.timed(steps)
+    tokens = wl["pipelines"] * wl["M"] * wl["seq"] * steps
+    return p, {"value": tokens / (ms * 1e-3), "unit": "tokens/s", "ms_per_step": ms / steps}
+
+
+def kernel_roofline(ctx, p, wl, steps, ms_step):
+    """Roofline of the dominant kernel (the one that moves the bytes):
+      N = 1 direct: copy_kernel, 2B of HBM per launch (read + write);
+      N = 1 ring:   push_ws_kernel (slot write) + recv_kernel (copy-out): 2B each;
+      N >= 2 zero-copy: recv_kernel (NVLink pull), B per launch;
+      N >= 2 ring:  push_ws_kernel (NVLink stores), B per launch.
+    achieved = algorithmic bytes per launch / the launch's duration, measured in an
+    instrumented eager pass of the same K steps with CUDA events on the launch streams."""
+    ppc = ctx.ppc
+    nb = wl["msg_bytes"]
+    peaks = measured_peaks()
+    n_rec0 = [len(c.trace()) for c in p.comms]
+    ms_instr = p.timed(steps, instrumented=True)
+    send_ms = [t for c in p.comms for t in c.kernel_times(0)]
+    recv_ms = [t for c in p.comms for t in c.kernel_times(1)]
+    recs = [r for c, n0 in zip(p.comms, n_rec0) for r in c.trace()[n0:] if r["kind"] == 1]
+    for c in p.comms:
+        c.set_trace(0)
+    if not ctx.distributed:
+        alg, peak, bound = 2 * nb, peaks.get("hbm_gbs", 6550.0), "hbm"
+        peak_src = ("MEASURED_PEAKS.json hbm_gbs (copy, read+write bytes)" if "hbm_gbs" in peaks
+                    else "fallback 6.55 TB/s")
+    else:
+        alg, peak, bound = nb, NVLINK_GBPS, "nvlink"
+        peak_src = "NVLink 5 nominal 900 GB/s per direction per GPU"
+    dom = recv_ms if (ctx.distributed and wl["zc"]) else send_ms
+    if not dom:
+        return None
+    per_launch = ctx.max_over_ranks(statistics.mean(dom))
+    roof = {"bound": bound, "peak": peak, "unit": "GB/s", "peak_source": peak_src,
+            "alg_bytes_per_launch": alg, "launches_timed": len(dom),
+            "event_launch_us": per_launch * 1e3,
+            "event_achieved": alg / (per_launch * 1e-3) / 1e9,
+            "instrumented_ms_per_step": ms_instr / steps}
+    # the same bytes over the headline (un-instrumented) step: every dominant launch of the
+    # step, both directions and all of this process's stages, back to back in the step time
+    per_step = alg * len(dom) / steps
+    roof["step_aggregate"] = {"bytes_per_step": per_step,
+                              "achieved": per_step / (ms_step * 1e-3) / 1e9,
+                              "frac": per_step / (ms_step * 1e-3) / 1e9 / peak}
+    if ctx.distributed and wl["zc"] and recs:
+        ph = ctx.max_over_ranks(statistics.mean((r["t_end_ns"] - r["t_start_ns"]) * 1e-3
+                                                for r in recs))
+        roof["pull_data_phase"] = {"avg_us": ph, "achieved": nb / (ph * 1e-6) / 1e9,
+                                   "frac": nb / (ph * 1e-6) / 1e9 / peak, "records": len(recs),
+                                   "timing": "%globaltimer in recv_kernel: publication seen -> "
+                                             "last CTA done (excludes the wait for the peer)"}
+    return roof
+
+
+def serialized_copy(ctx, wl, steps):
+    """N = 1 direct mode with every hand-off copy on ONE transfer queue (PPC_LOCAL_QUEUE=1),
+    so copy_kernel launches never overlap: per-launch CUDA events then time the kernel alone
+    (the duration ncu's serialised launch list shows).  Returns (us per launch, launches)."""
+    os.environ["PPC_LOCAL_QUEUE"] = "1"
+    try:
+        p = Pipeline(ctx, {**wl, "graph": False})
+        p.step()
+        p.timed(steps, instrumented=True)
+        ms = [t for c in p.comms for t in c.kernel_times(0)]
+        p.close()
+    finally:
+        os.environ.pop("PPC_LOCAL_QUEUE", None)
+    return (statistics.median(ms) * 1e3 if ms else None), len(ms)
+
+
+def e2e_leg(ctx, p, wl, steps):
+    """The same step through the C-ABI with pinned HOST X / G in and HOST Y / DX out: the
+    host<->device copies run inside the timed region (libppc's staging streams)."""
+    torch, ppc = ctx.torch, ctx.ppc
+    nb, M = wl["msg_bytes"], wl["M"]
+    hb = lambda: [torch.empty(nb, dtype=torch.uint8).pin_memory() for _ in range(M)]
+    hX = {s: hb() for s in p.X}
+    hG = {s: hb() for s in p.G}
+    hY = {s: hb() for s in p.Y}
+    hDX = {s: hb() for s in p.DX}
+    for s in hX:
+        for m in range(M):
+            hX[s][m].copy_(p.X[s][m].cpu())
+    for s in hG:
+        for m in range(M):
+            hG[s][m].copy_(p.G[s][m].cpu())
+    args = [ppc.StepArgs(M, nb, nb, x=hX.get(s), g=hG.get(s), y=hY.get(s), dx=hDX.get(s))
+            for s in p.stages]
+    K2 = max(3, min(steps, 10))
+    p.step(args)
+    ctx.barrier()
+    e0 = [torch.cuda.Event(enable_timing=True) for _ in p.stages]
+    e1 = [torch.cuda.Event(enable_timing=True) for _ in p.stages]
+    for e, st in zip(e0, p.streams):
+        e.record(st)
+    for _ in range(K2):
+        p.step(args)
+    for e, st in zip(e1, p.streams):
+        e.record(st)
+    ctx.barrier()
+    ms = ctx.max_over_ranks(max(a.elapsed_time(b) for a, b in zip(e0, e1)))
+    h2d = int(ctx.sum_over_ranks((len(hX) + len(hG)) * M * nb))
+    d2h = int(ctx.sum_over_ranks((len(hY) + len(hDX)) * M * nb))
+    ok = True                       # identity stages: Y_m = X_m, DX_m = G_m, every m
+    ref = torch.empty(nb, dtype=torch.uint8, device=ctx.dev)
+    for outs, d in ((hY, 0), (hDX, 1)):
+        for s in outs:
+            for m in range(M):
+                ppc.fill_payload(ref, nb, 42, 0, 0xFF, d, m)
+                ok &= bool(torch.equal(outs[s][m].to(ctx.dev), ref))
+    return {"value": wl["pipelines"] * M * wl["seq"] * K2 / (ms * 1e-3), "unit": "tokens/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms / K2,
+            "steps": K2, "outputs_checked": ctx.all_true(ok),
+            "roofline": pcie_roofline(ctx.world, h2d / ctx.world, d2h / ctx.world, ms / K2)}
+
+
+def b1_arm(ctx, wl, steps=3, channels=4, chunk=4 << 20):
+    """CPU-Forwarding baseline B1 (libppcb, P:L37/P:L47/P:L163): D2H into a pinned /dev/shm
+    ring, per-chunk host flags, H2D at the receiver, `channels` host threads — the same
+    1F1B step (identity stages, the headline's buffers) between the two stages of every
+    PP = 2 pipeline; N = 1: both virtual stages in this process, one host thread stepping
+    them in dependency order.  Host wall clock (the calls block), max over ranks."""
+    torch, ppc = ctx.torch, ctx.ppc
+    from paper_2602_18007_b200.cpufwd import CpuFwdLink
+    if wl["pp"] != 2:
+        return None
+    nb, M = wl["msg_bytes"], wl["M"]
+    dev = ctx.dev
+    s = torch.cuda.current_stream()
+    X = [torch.empty(nb, dtype=torch.uint8, device=dev) for _ in range(M)]
+    G = [torch.empty(nb, dtype=torch.uint8, device=dev) for _ in range(M)]
+    OUT = {0: [torch.empty(nb, dtype=torch.uint8, device=dev) for _ in range(M)],
+           1: [torch.empty(nb, dtype=torch.uint8, device=dev) for _ in range(M)]}
+    for m in range(M):
+        ppc.fill_payload(X[m], nb, 42, 0, 0xFF, 0, m)
+        ppc.fill_payload(G[m], nb, 42, 0, 0xFF, 1, m)
+    K = 2
+    if ctx.distributed:
+        pids = [None] * ctx.world
+        ctx.dist.all_gather_object(pids, os.getpid())
+        dpw = ctx.world // 2                    # rank = pp_i * dp + dp_i (pp = 2, tp = 1)
+        st = ctx.rank // dpw                    # stage of this rank; its pipeline = dp_i
+        lead = pids[ctx.rank % dpw]
+        fwd = CpuFwdLink(f"b1f_{lead}", st == 0, nb, chunk, K, channels, dev)
+        bwd = CpuFwdLink(f"b1b_{lead}", st == 1, nb, chunk, K, channels, dev)
+        ctx.dist.barrier()
+        fwd.connect()
+        bwd.connect()
+        ctx.dist.barrier()
+        ops = ppc.schedule_1f1b(2, st, M)
+
+        def step():
+            for kind, m in ops:
+                if st == 0:
+                    (fwd.send(X[m], nb, m, s) if kind == "F" else bwd.recv(OUT[0][m], nb, m, s))
+                else:
+                    (fwd.recv(OUT[1][m], nb, m, s) if kind == "F" else bwd.send(G[m], nb, m, s))
+        links = [fwd, bwd]
+    else:
+        tag = os.getpid()
+        fs = CpuFwdLink(f"b1f_{tag}", True, nb, chunk, K, channels, dev)
+        fr = CpuFwdLink(f"b1f_{tag}", False, nb, chunk, K, channels, dev)
+        bs = CpuFwdLink(f"b1b_{tag}", True, nb, chunk, K, channels, dev)
+        br = CpuFwdLink(f"b1b_{tag}", False, nb, chunk, K, channels, dev)
+        for ln in (fs, fr, bs, br):
+            ln.connect()
+        links = [fs, fr, bs, br]
+        ops = [ppc.schedule_1f1b(2, st, M) for st in (0, 1)]
+
+        def step():
+            # one host thread, both stages: run each stage's next op when its input message
+            # exists and a send has a free slot (blocking calls never wait on the other stage)
+            i = [0, 0]
+            sent = {0: 0, 1: 0}                 # per direction
+            recvd = {0: 0, 1: 0}
+            while i[0] < len(ops[0]) or i[1] < len(ops[1]):
+                prog = False
+                for stg in (0, 1):
+                    if i[stg] >= len(ops[stg]):
+                        continue
+                    kind, m = ops[stg][i[stg]]
+                    d = 0 if kind == "F" else 1
+                    is_send = (stg == 0 and d == 0) or (stg == 1 and d == 1)
+                    if is_send:
+                        if sent[d] - recvd[d] >= K:
+                            continue
+                        (fs.send(X[m], nb, m, s) if d == 0 else bs.send(G[m], nb, m, s))
+                        sent[d] += 1
+                    else:
+                        if recvd[d] >= sent[d]:
+                            continue
+                        (fr.recv(OUT[1][m], nb, m, s) if d == 0 else br.recv(OUT[0][m], nb, m, s))
+                        recvd[d] += 1
+                    i[stg] += 1
+                    prog = True
+                if not prog:
+                    raise RuntimeError("B1 step made no progress")
+    step()
+    ctx.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    torch.cuda.synchronize()
+    dt = ctx.max_over_ranks(time.perf_counter() - t0)
+    ok = True
+    st_here = [0, 1] if not ctx.distributed else [ctx.rank // (ctx.world // 2)]
+    for m in range(M):
+        if 1 in st_here:
+            ok &= bool(torch.equal(OUT[1][m], X[m]))
+        if 0 in st_here:
+            ok &= bool(torch.equal(OUT[0][m], G[m]))
+    ctx.barrier()
+    for ln in links:
+        ln.destroy()
+    tokens = wl["pipelines"] * M * wl["seq"] * steps
+    return {"impl": f"B1 CPU-Forwarding (libppcb): D2H -> pinned /dev/shm ring -> H2D, "
+                    f"{channels} channel threads, {chunk >> 20} MiB chunks, K={K}",
+            "value": tokens / dt, "unit": "tokens/s", "ms_per_step": 1e3 * dt / steps,
+            "steps": steps, "outputs_checked": ctx.all_true(ok),
+            "timing": "host wall clock (blocking calls), max over ranks"}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
-    import torch
-    import torch.distributed as dist
-    import paper_2602_18007_b200 as ppc
+    ctx = Ctx()
+    torch, ppc = ctx.torch, ctx.ppc
+    wl = resolve(args, ctx.world)
+    launches0 = ppc.launch_count()
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    distributed = world > 1
-    if distributed:
-        torch.cuda.set_device(local)
-        dist.init_process_group("gloo")
-    else:
-        torch.cuda.set_device(0)
-    dev = torch.cuda.current_device()
-    if args.zc < 0:
-        args.zc = 1 if args.pp == 2 else 0
-    if args.engine == "ce":
-        args.graph = 0        # the CE engine's host-resolved slots are not graph-capturable
-    if not args.chunk:
-        # tuned on 2x B200 (profiles/r1_tune_step_ws.jsonl): 512 KiB chunks x 64 CTAs
-        # zero-copy pulls: 256 KiB grain; ring push: 512 KiB (profiles/r11_tune_zero_copy.jsonl)
-        args.chunk = ((256 if args.zc else 512) << 10) if distributed else (128 << 10)
-    S = args.pp
-    nbytes = args.seq * args.hidden * 2
-    M = args.M
-    engine = {"sm": ppc.ENGINE_SM, "ce": ppc.ENGINE_CE, "pull": ppc.ENGINE_PULL}[args.engine]
-    cfg = ppc.make_config(tp=1, pp=S, dp=max(1, world // S) if distributed else 1,
-                          max_msg_bytes=nbytes, ring_slots=args.slots, channels=args.channels,
-                          chunk_bytes=args.chunk, engine=engine, cta_per_channel=args.cta,
-                          trace=3)
-    if distributed:
-        if world % S:
-            raise SystemExit(f"--gpus {world} is not a multiple of pp={S}")
-        comms = [ppc.connect_distributed(cfg, rank, world, local, with_nccl=False)]
-        stages = [comms[0].group(ppc.GROUP_PP)[0].index(rank)]
-        pipelines = world // S
-    else:
-        comms = ppc.virtual_stages(cfg, dev)
-        stages = list(range(S))
-        pipelines = 1
-
-    def bufs():
-        return [torch.empty(nbytes, dtype=torch.uint8, device=dev) for _ in range(M)]
-
-    X = {s: bufs() for s in stages if s == 0}
-    G = {s: bufs() for s in stages if s == S - 1}
-    Y = {s: bufs() for s in stages if s == S - 1}
-    DX = {s: bufs() for s in stages if s == 0}
-    for s in stages:
-        for m in range(M):
-            if s in X:
-                ppc.fill_payload(X[s][m], nbytes, 42, 0, 0xFF, 0, m)
-            if s in G:
-                ppc.fill_payload(G[s][m], nbytes, 42, 0, 0xFF, 1, m)
-    args_dev = [ppc.StepArgs(M, nbytes, nbytes, x=X.get(s), g=G.get(s), y=Y.get(s),
-                             dx=DX.get(s)) for s in stages]
-    streams = [torch.cuda.Stream() for _ in stages]
-    if distributed and args.zc:
-        # zero-copy: the stage inputs X / G are registered send buffers; receivers pull them
-        ppc.register_tensors(comms[0], [t for s in stages for t in X.get(s, []) + G.get(s, [])])
-
-    graph = [None]
-
-    def one_step(a=None, eager=False):
-        if graph[0] is not None and a is None and not eager:
-            graph[0].launch()
-            return
-        a = a or args_dev
-        if distributed:
-            ppc.step_1f1b(comms[0], a[0], streams[0])
-        else:
-            ppc.step_1f1b_local(comms, a, streams)
-
-    def barrier():
-        torch.cuda.synchronize()
-        if distributed:
-            dist.barrier()
-
-    def max_over_ranks(v):
-        if not distributed:
-            return v
-        t = torch.tensor([v], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    one_step(eager=True)                 # allocates the step buffers
-    barrier()
-    if args.graph:                       # the whole step as one CUDA graph per process
-        graph[0] = ppc.StepGraph(comms, args_dev, streams)
+    # ---- headline: K steps, un-instrumented, clocks sampled during the timed region
+    p = Pipeline(ctx, wl)
     for _ in range(args.warmup):
-        one_step()
-    barrier()
-
-    def timed_region(instrumented: bool):
-        """K steps between barriers + synchronize; CUDA events on every stage stream (the
-        launch stream for graph replays); max over ranks.  instrumented: eager steps with
-        CUDA-event pairs around every transfer launch."""
-        for c in comms:
-            c.set_trace(2 if instrumented else 0)
-            c.kernel_times(0), c.kernel_times(1)
-        sts = streams[:1] if (graph[0] is not None and not instrumented) else streams
-        ev0 = [torch.cuda.Event(enable_timing=True) for _ in sts]
-        ev1 = [torch.cuda.Event(enable_timing=True) for _ in sts]
-        barrier()
-        for e, st in zip(ev0, sts):
-            e.record(st)
-        for _ in range(args.steps):
-            one_step(eager=instrumented)
-        for e, st in zip(ev1, sts):
-            e.record(st)
-        barrier()
-        return max_over_ranks(max(a.elapsed_time(b) for a, b in zip(ev0, ev1)))
-
-    # ---- headline timed region (no instrumentation), clocks sampled during it
-    sampler = ClockSampler(dev)
+        p.step()
+    ctx.barrier()
+    sampler = ClockSampler(ctx.dev)
     sampler.start()
-    ms_total = timed_region(False)
+    l0 = ppc.launch_count()
+    ms_total = p.timed(args.steps)
+    launches = int(ctx.sum_over_ranks(ppc.launch_count() - l0))
     clocks = sampler.stop()
     ms_step = ms_total / args.steps
-    tokens = pipelines * M * args.seq * args.steps
+    tokens = wl["pipelines"] * wl["M"] * wl["seq"] * args.steps
     value = tokens / (ms_total * 1e-3)
-    # ---- the same K steps again with per-launch CUDA events for the kernel roofline
-    n_rec0 = [len(c.trace()) for c in comms]
-    ms_instr = timed_region(True)
-    push_ms = [t for c in comms for t in c.kernel_times(0)]
-    recv_ms = [t for c in comms for t in c.kernel_times(1)]
-    # device-side %globaltimer records of the receives of that pass: a zero-copy receive's
-    # record starts when the publication is seen, so t_end - t_start is its pull (data phase)
-    recv_recs = [r for c, n0 in zip(comms, n_rec0) for r in c.trace()[n0:] if r["kind"] == 1]
-    for c in comms:
-        c.set_trace(0)
-    n_launch_local = len(push_ms) + len(recv_ms)
-    n_launch = n_launch_local
-    if distributed:
-        t = torch.tensor([n_launch_local], dtype=torch.float64)
-        dist.all_reduce(t)
-        n_launch = int(t.item())
+    outputs_ok = p.outputs_ok()
+    roof = kernel_roofline(ctx, p, wl, args.steps, ms_step)
+    if roof is not None and not ctx.distributed:
+        us, n = serialized_copy(ctx, wl, args.steps)
+        roof.update({"kernel": "ppc::copy_kernel (virtual-stage SIMT hand-off)",
+                     "achieved": roof["alg_bytes_per_launch"] / (us * 1e-6) / 1e9,
+                     "avg_launch_us": us, "launches_serialized": n,
+                     "timed_region": "copy_kernel launches of K eager steps on one transfer "
+                                     "queue (no overlap), CUDA events per launch (median)",
+                     "traffic": ncu_traffic("copy_n1")})
+    elif roof is not None and wl["zc"]:
+        ph = roof.get("pull_data_phase", {})
+        roof.update({"kernel": "ppc::recv_kernel (zero-copy NVLink pull into the user buffer)",
+                     "achieved": ph.get("achieved", roof["event_achieved"]),
+                     "avg_launch_us": ph.get("avg_us", roof["event_launch_us"]),
+                     "timed_region": "per-launch data phase (%globaltimer, publication seen -> "
+                                     "last CTA); event_* = CUDA events around the launch, "
+                                     "which include the wait for the peer's publication",
+                     "traffic": ncu_traffic("recv_n2")})
+    elif roof is not None:
+        roof.update({"kernel": "ppc::push_ws_kernel (SM push over NVLink)",
+                     "achieved": roof["event_achieved"], "avg_launch_us": roof["event_launch_us"],
+                     "timed_region": "CUDA events around every push launch (instrumented pass)",
+                     "traffic": ncu_traffic("push_n2")})
+    if roof is not None:
+        roof["frac"] = roof["achieved"] / roof["peak"]
 
-    # dominant kernel: the one that moves the bytes — N=1: the hand-off copy; N>=2 zero-copy:
-    # the receiver's NVLink pull (recv_kernel; its launch also spans the wait for the peer's
-    # publication); N>=2 ring: the SM push
-    zc_dom = distributed and bool(args.zc)
-    dom_ms = recv_ms if zc_dom else push_ms
-    avg_push_ms = statistics.mean(dom_ms) if dom_ms else float("nan")
-    avg_push_ms = max_over_ranks(avg_push_ms)
-    peaks = measured_peaks()
-    if distributed:
-        alg = nbytes                                  # bytes that cross NVLink per launch
-        peak, unit, bound = NVLINK_GBPS, "GB/s", "nvlink"
-        peak_src = "NVLink 5 nominal 900 GB/s per direction (guide measured peer copy 770)"
-    else:
-        alg = 2 * nbytes                              # HBM read + write per launch
-        peak = peaks.get("hbm_gbs", 6650.0)
-        unit, bound = "GB/s", "hbm"
-        peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
-    achieved = alg / (avg_push_ms * 1e-3) / 1e9
-    if not distributed:
-        if os.environ.get("PPC_COPY_TMA_CTAS", "0") != "0":
-            kname, tkey = "ppc::copy_tma_kernel (virtual-stage TMA bulk hand-off)", "copy_tma_n1"
-        else:
-            kname, tkey = "ppc::copy_kernel (virtual-stage SIMT hand-off)", "copy_n1"
-    elif zc_dom:
-        kname = ("ppc::recv_kernel (zero-copy NVLink pull into the user buffer; CUDA events "
-                 "on its stream, so the launch time includes the wait for the publication)")
-        tkey = "recv_n2"
-    else:
-        kname, tkey = "ppc::push_ws_kernel (SM push over NVLink)", "push_n2"
-    roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
-            "frac": achieved / peak, "traffic": ncu_traffic(tkey),
-            "kernel": kname, "alg_bytes_per_launch": alg,
-            "avg_launch_us": avg_push_ms * 1e3, "launches_timed": len(dom_ms),
-            "peak_source": peak_src,
-            "timed_region": "second pass of the same K steps with per-launch CUDA events "
-                            f"(step {ms_instr / args.steps:.3f} ms instrumented vs {ms_step:.3f} plain)",
-            "step_aggregate": {"bytes_per_step": alg * len(dom_ms) / max(1, args.steps),
-                               "achieved": alg * len(dom_ms) / (ms_instr * 1e-3) / 1e9,
-                               "achieved_plain": alg * len(dom_ms) / max(1, args.steps)
-                                                 / (ms_step * 1e-3) / 1e9,
-                               "frac_plain": alg * len(dom_ms) / max(1, args.steps)
-                                             / (ms_step * 1e-3) / 1e9 / peak,
-                               "note": "this process's transfer launches of the step (both "
-                                       "directions, concurrent) over the instrumented step "
-                                       "time (achieved) and over the un-instrumented headline "
-                                       "step time (achieved_plain)"},
-            "send_avg_launch_us": (statistics.mean(push_ms) * 1e3) if push_ms else None,
-            "recv_avg_launch_us": (statistics.mean(recv_ms) * 1e3) if recv_ms else None}
-    # launches of the dominant kernel overlap (the F and B transfers of a 1F1B step run
-    # concurrently and share the bandwidth), so per-launch "achieved" is ~1/concurrency of
-    # what the kernel class moves; report the measured overlap beside it
-    if dom_ms and ms_instr > 0:
-        conc = sum(dom_ms) / ms_instr        # this process's launches (all its stages)
-        roof["concurrency"] = conc
-        roof["frac_x_concurrency"] = roof["frac"] * conc
-    if distributed and args.zc and recv_recs:
-        phase_us = statistics.mean((r["t_end_ns"] - r["t_start_ns"]) * 1e-3 for r in recv_recs)
-        phase_us = max_over_ranks(phase_us)
-        roof["zero_copy_pull_data_phase"] = {
-            "avg_us": phase_us, "achieved": nbytes / (phase_us * 1e-6) / 1e9, "unit": "GB/s",
-            "frac": nbytes / (phase_us * 1e-6) / 1e9 / peak, "records": len(recv_recs),
-            "timing": "%globaltimer stamps in recv_kernel: publication seen -> last CTA done"}
-    boundary_gbps = 2 * M * nbytes * pipelines * (S - 1) * args.steps / (ms_total * 1e-3) / 1e9
+    e2e = None if args.no_e2e else e2e_leg(ctx, p, wl, args.steps)
+    p.close()
 
-    # ---- e2e: the same step through the C-ABI with pinned HOST inputs / outputs
-    e2e = None
-    if not args.no_e2e:
-        def hbufs():
-            return [torch.empty(nbytes, dtype=torch.uint8).pin_memory() for _ in range(M)]
-        hX = {s: hbufs() for s in X}
-        hG = {s: hbufs() for s in G}
-        hY = {s: hbufs() for s in Y}
-        hDX = {s: hbufs() for s in DX}
-        for s in hX:
-            for m in range(M):
-                hX[s][m].copy_(X[s][m].cpu())
-        for s in hG:
-            for m in range(M):
-                hG[s][m].copy_(G[s][m].cpu())
-        args_host = [ppc.StepArgs(M, nbytes, nbytes, x=hX.get(s), g=hG.get(s), y=hY.get(s),
-                                  dx=hDX.get(s)) for s in stages]
-        K2 = max(3, min(args.steps, 10))
-        one_step(args_host)
-        barrier()
-        e0 = [torch.cuda.Event(enable_timing=True) for _ in stages]
-        e1 = [torch.cuda.Event(enable_timing=True) for _ in stages]
-        for e, st in zip(e0, streams):
-            e.record(st)
-        for _ in range(K2):
-            one_step(args_host)
-        for e, st in zip(e1, streams):
-            e.record(st)
-        barrier()
-        ms_e2e = max_over_ranks(max(a.elapsed_time(b) for a, b in zip(e0, e1)))
-        h2d = (len(hX) + len(hG)) * M * nbytes
-        d2h = (len(hY) + len(hDX)) * M * nbytes
-        if distributed:
-            t = torch.tensor([h2d, d2h], dtype=torch.float64)
-            dist.all_reduce(t)
-            h2d, d2h = int(t[0]), int(t[1])
-        ok = all(torch.equal(hY[s][m], X[0][m].cpu()) for s in hY for m in (0, M - 1)) \
-            if (hY and 0 in X) else None
-        e2e = {"value": pipelines * M * args.seq * K2 / (ms_e2e * 1e-3), "unit": "tokens/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "ms_per_step": ms_e2e / K2, "steps": K2, "outputs_checked": ok,
-               "roofline": pcie_roofline(world, h2d / world, d2h / world, ms_e2e / K2)}
-        for c in comms:
-            c.kernel_times(0), c.kernel_times(1)
+    # ---- N = 1: the intra-device ring (push into the slot + chunk flags + copy-out)
+    ring = None
+    if not ctx.distributed and not args.no_ring:
+        pr, ring = measure(ctx, wl, args.steps, args.warmup, local_direct=False)
+        ring["outputs_checked"] = pr.outputs_ok()
+        rr = kernel_roofline(ctx, pr, wl, args.steps, ring["ms_per_step"])
+        pr.close()
+        ring["config"] = "PPC_LOCAL_DIRECT=0: push_ws_kernel writes the ring slot (chunk flags), " \
+                         "recv_kernel copies it out; CUDA graph"
+        if rr:
+            ring["roofline"] = {k: rr[k] for k in ("bound", "peak", "unit", "step_aggregate",
+                                                   "event_launch_us", "event_achieved")}
+            # every message moves 4B of HBM on the ring (slot write + copy-out)
+            msgs = 2 * wl["M"]
+            ring["hbm_gbps_step"] = 4 * wl["msg_bytes"] * msgs / (ring["ms_per_step"] * 1e-3) / 1e9
+            ring["hbm_frac_step"] = ring["hbm_gbps_step"] / rr["peak"]
+
+    # ---- north-star configurations beside the headline (as many as the GPUs allow)
+    extra = {}
+    if not args.no_extra:
+        for name in EXTRA.get(ctx.world, []):
+            wx = resolve(args, ctx.world, name)
+            px, r = measure(ctx, wx, max(3, args.steps // 2), max(3, args.warmup))
+            r["outputs_checked"] = px.outputs_ok()
+            px.close()
+            r["config"] = config_dict(wx, ctx.world)
+            extra[name] = r
+
+    # ---- CPU-Forwarding B1 on the headline workload
+    b1 = None
+    if not args.no_b1:
+        try:
+            b1 = b1_arm(ctx, wl)
+        except Exception as e:          # the baseline must not sink the line
+            b1 = {"error": repr(e)[:200]}
 
     cpu = None
-    if rank == 0 and not distributed and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args, nbytes)
+    if ctx.rank == 0 and not ctx.distributed and not args.no_cpu_baseline:
+        cpu = cpu_baseline(wl)
 
-    bad = [c.poll() for c in comms if c.poll() != 0]
-    if rank == 0:
-        msg_us = nbytes / (NVLINK_GBPS * 1e3)
+    if ctx.rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ctx.world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-            "data": "synthetic", "config": workload_config(args, pipelines, not distributed),
-            "boundary_gbps": boundary_gbps,
-            "step_roofline_us_pp2": (M + 1) * msg_us if S == 2 else None,
-            "frac_of_step_roofline": ((M + 1) * msg_us / (ms_step * 1e3)) if S == 2 else None,
+            "data": "synthetic",
+            "config": config_dict(wl, ctx.world), "outputs_checked": outputs_ok,
+            "boundary_gbps": 2 * wl["M"] * wl["msg_bytes"] * wl["pipelines"] * (wl["pp"] - 1)
+                             / (ms_step * 1e-3) / 1e9,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
-            "gpu_launches": n_launch, "errors": [ppc.STATUS[b] for b in bad],
+            "gpu_launches": launches, "cpu_forwarding": b1,
         }
+        if b1 and "value" in b1:
+            line["device_direct_vs_cpu_forwarding"] = value / b1["value"]
+        if ring:
+            line["intra_device_ring"] = ring
+        if extra:
+            line["north_star_configs"] = extra
+        if ctx.distributed and wl["pp"] == 2:
+            t_msg = wl["msg_bytes"] / (NVLINK_GBPS * 1e3)
+            line["step_roofline"] = {"us": (wl["M"] + 1) * t_msg,
+                                     "frac": (wl["M"] + 1) * t_msg / (ms_step * 1e3),
+                                     "model": "PP2 comm-only critical path (M+1) x t_msg at "
+                                              "900 GB/s (DESIGN.md R5; oracle O2)"}
         print(json.dumps(line), flush=True)
-    barrier()
-    if graph[0] is not None:
-        graph[0].destroy()
-    for c in comms:
-        c.disconnect()
-    if distributed:
-        dist.barrier()
-    for c in comms:
-        c.destroy()
-    if distributed:
-        dist.destroy_process_group()
+    ctx.barrier()
+    if ctx.distributed:
+        ctx.dist.destroy_process_group()
 
 
 if __name__ == "__main__":

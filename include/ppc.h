@@ -112,6 +112,17 @@ typedef struct {
                                    consecutive sends on one stream overlap; the caller keeps
                                    the buffer unchanged until ppc_pp_wait_consumed (like an
                                    MPI_Isend / MPI_Wait pair).  0: rendezvous (default)        */
+  int local_spin;               /* comms of ONE process (virtual stages, ppc_connect with blobs
+                                   of the same pid): 0 => CUDA events order the stages (the
+                                   virtual-stage mode, ppc_step_1f1b_local); 1 => the comms
+                                   behave exactly like one process per GPU — device flag /
+                                   credit / header spins with .sys scope, zero-copy
+                                   registrations, publication, TP gathers, the per-rank step
+                                   driver ppc_step_1f1b on each comm (the host never blocks,
+                                   so S comms are stepped one after another from one thread).
+                                   Spinning grids of stages sharing a GPU are capped at 8
+                                   CTAs so every stage stays resident.  Lets one GPU exercise
+                                   the whole cross-process protocol (tests, smoke)          */
 } ppc_config_t;
 
 typedef struct ppc_comm ppc_comm_t;
@@ -314,6 +325,10 @@ ppc_status_t ppc_set_trace(ppc_comm_t* c, int trace);
 ppc_status_t ppc_disconnect(ppc_comm_t* c);        /* phase 1: close peer handles, NCCL    */
 ppc_status_t ppc_destroy(ppc_comm_t* c);           /* phase 2 (after a caller barrier)     */
 const char* ppc_status_str(ppc_status_t st);
+/* Kernels libppc enqueued in this process so far (transport, stage proxy and fill kernels;
+ * a CUDA graph's kernel nodes count once per ppc_graph_launch).  Copy-engine copies are not
+ * kernels and are not counted.  Thread-safe, monotone. */
+unsigned long long ppc_launch_count(void);
 /* sizeof of the ABI structs, for bindings to check their layouts: which = 0 ppc_config_t,
  * 1 ppc_step_t, 2 ppc_record_t, 3 ppc_op_t, 4 ppc_slot_t; 0 for any other value. */
 size_t ppc_struct_size(int which);

@@ -48,7 +48,8 @@ class Config(C.Structure):
     _fields_ = [("tp", C.c_int), ("pp", C.c_int), ("dp", C.c_int),
                 ("max_msg_bytes", C.c_size_t), ("ring_slots", C.c_int), ("channels", C.c_int),
                 ("chunk_bytes", C.c_size_t), ("engine", C.c_int), ("cta_per_channel", C.c_int),
-                ("timeout_ns", C.c_ulonglong), ("trace", C.c_int), ("zc_async", C.c_int)]
+                ("timeout_ns", C.c_ulonglong), ("trace", C.c_int), ("zc_async", C.c_int),
+                ("local_spin", C.c_int)]
 
 
 class Op(C.Structure):
@@ -124,7 +125,13 @@ _disconnect = _sig("ppc_disconnect", _i, [_vp])
 _destroy = _sig("ppc_destroy", _i, [_vp])
 _status_str = _sig("ppc_status_str", C.c_char_p, [_i])
 _fill = _sig("ppc_fill_payload", _i, [_vp, _sz, _i, _i, _i, _i, _ll, _vp])
+_launch_count = _sig("ppc_launch_count", C.c_ulonglong, [])
 STAGE_XOR = C.cast(_lib.ppc_stage_xor, C.c_void_p).value   # ppc_stage_fn address
+
+
+def launch_count() -> int:
+    """Kernels libppc enqueued in this process so far (ppc_launch_count)."""
+    return int(_launch_count())
 
 
 def lib_path() -> str:
@@ -161,9 +168,9 @@ def _stream(s):
 
 def make_config(tp=1, pp=2, dp=1, max_msg_bytes=32 << 20, ring_slots=0, channels=1,
                 chunk_bytes=1 << 20, engine=ENGINE_SM, cta_per_channel=0, timeout_ns=0,
-                trace=0, zc_async=0) -> Config:
+                trace=0, zc_async=0, local_spin=0) -> Config:
     return Config(tp, pp, dp, max_msg_bytes, ring_slots, channels, chunk_bytes, engine,
-                  cta_per_channel, timeout_ns, trace, zc_async)
+                  cta_per_channel, timeout_ns, trace, zc_async, local_spin)
 
 
 def schedule_1f1b(S: int, s: int, M: int):
@@ -404,13 +411,31 @@ def fill_payload(buf, nbytes=None, seed=42, step=0, boundary=0, direction=0, mb=
 def virtual_stages(cfg: Config, device=0):
     """S = cfg.pp virtual stages of one pipeline in this process (K11 path).  `device` is one
     device index for all stages, or a list with one device per stage (stages on different
-    GPUs of one process: NVLink transfers ordered by events, used for profiling)."""
-    devs = list(device) if isinstance(device, (list, tuple)) else [device] * cfg.pp
-    comms = [Comm(cfg, cfg.pp, r, devs[r]) for r in range(cfg.pp)]
+    GPUs of one process: NVLink transfers ordered by events, used for profiling).  With
+    cfg.local_spin the stages run the cross-process protocol instead (device spins; step
+    each with step_1f1b)."""
+    return local_comms(cfg, device)
+
+
+def local_comms(cfg: Config, device=0):
+    """Every rank of the cfg grid (tp * pp * dp comms, rank order) in this process, blobs
+    exchanged in-process.  `device`: one index for all ranks or a list per rank."""
+    world = cfg.tp * cfg.pp * cfg.dp
+    devs = list(device) if isinstance(device, (list, tuple)) else [device] * world
+    comms = [Comm(cfg, world, r, devs[r]) for r in range(world)]
     blobs = [c.export() for c in comms]
     for c in comms:
         c.connect(blobs)
     return comms
+
+
+def register_local(comms, tensors_by_rank):
+    """register_tensors for comms of one process: tensors_by_rank[r] are rank r's send
+    buffers; every comm imports every registration (non-neighbours ignore them)."""
+    blobs = [comms[r].register(t) for r in range(len(comms)) for t in (tensors_by_rank[r] or [])]
+    for c in comms:
+        for b in blobs:
+            c.register_import(b)
 
 
 def connect_distributed(cfg: Config, rank: int, world: int, device: int, pg=None,

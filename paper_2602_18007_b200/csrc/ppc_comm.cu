@@ -197,11 +197,16 @@ ppc_status_t ppc_create(const ppc_config_t* cfg, int world, int rank, int cuda_d
     if (preload_kernels() != cudaSuccess) return fail(PPC_ERR_CUDA);   // no lazy loads later
     if (cudaMalloc(&c->arena, c->lay.total) != cudaSuccess) return fail(PPC_ERR_CUDA);
     if (cudaMemset(c->arena, 0, c->lay.total) != cudaSuccess) return fail(PPC_ERR_CUDA);
-    if (cudaHostAlloc(&c->err_host, sizeof(ErrWord), cudaHostAllocMapped) != cudaSuccess)
+    if (cudaHostAlloc(&c->err_host, sizeof(ErrHost), cudaHostAllocMapped) != cudaSuccess)
       return fail(PPC_ERR_CUDA);
-    memset(c->err_host, 0, sizeof(ErrWord));
-    if (cudaHostGetDevicePointer((void**)&c->err_dev, c->err_host, 0) != cudaSuccess)
-      return fail(PPC_ERR_CUDA);
+    memset(c->err_host, 0, sizeof(ErrHost));
+    {
+      ErrWord w{};
+      if (cudaHostGetDevicePointer((void**)&w.host, c->err_host, 0) != cudaSuccess ||
+          cudaMalloc(&c->err_dev, sizeof(ErrWord)) != cudaSuccess ||
+          cudaMemcpy(c->err_dev, &w, sizeof(w), cudaMemcpyHostToDevice) != cudaSuccess)
+        return fail(PPC_ERR_CUDA);
+    }
     if (cudaIpcGetMemHandle(&b.ipc, c->arena) != cudaSuccess) return fail(PPC_ERR_CUDA);
     if (cudaDeviceGetPCIBusId(b.busid, sizeof(b.busid), cuda_device) != cudaSuccess)
       return fail(PPC_ERR_CUDA);
@@ -306,12 +311,21 @@ ppc_status_t ppc_connect(ppc_comm_t* c, const void* all_blobs, size_t blob_bytes
       if (B[nb].pid == c->blob.pid && B[nb].host_hash == c->blob.host_hash) ++same; else ++cross;
     }
     if (same && cross) return PPC_ERR_INVALID_ARG;
-    c->local_mode = same > 0;
+    // cfg.local_spin: same-process neighbours run the cross-process protocol (device spins)
+    c->local_mode = same > 0 && !c->cfg.local_spin;
     // virtual stages may also sit on different GPUs of this process (used to profile the
     // NVLink push without cross-process spins): enable peer access, keep .sys scope
     c->sys_scope = !c->local_mode;
+    // a spinning grid must never starve the peer it waits for: stages of this process that
+    // share our GPU get small spinning grids (other processes time-slice the GPU instead)
+    for (int r = 0; r < c->world; ++r)
+      if (r != c->rank && B[r].pid == c->blob.pid && B[r].host_hash == c->blob.host_hash &&
+          B[r].device == c->device)
+        c->spin_cap = 8;
     for (int nb : {prev, next}) {
-      if (nb < 0 || !c->local_mode || B[nb].device == c->device) continue;
+      if (nb < 0 || B[nb].pid != c->blob.pid || B[nb].host_hash != c->blob.host_hash ||
+          B[nb].device == c->device)
+        continue;
       c->sys_scope = true;
       cudaError_t e = cudaDeviceEnablePeerAccess(B[nb].device, 0);
       if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
@@ -778,7 +792,7 @@ ppc_status_t ppc_pp_recv_gather(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t to
   a.done = h.i_done + slot;
   a.err = c->err_dev;
   a.timeout_ns = c->timeout_ns;
-  const int grid = (int)std::max<uint32_t>(1, std::min<uint32_t>(a.tp * a.n_chunks, 64));
+  const int grid = (int)std::max<uint32_t>(1, std::min<uint32_t>(a.tp * a.n_chunks, (uint32_t)c->spin_cap));
   if (ppc_status_t ts = time_mark(c, 1, s, true)) return ts;
   CK(launch_gather(a, grid, s));
   if (ppc_status_t ts = time_mark(c, 1, s, false)) return ts;
@@ -946,7 +960,7 @@ ppc_status_t ppc_hetero_allreduce(ppc_comm_t* c, void* buf, size_t count, int nc
 ppc_status_t ppc_error_info(ppc_comm_t* c, unsigned* seq, unsigned* info) {
   if (!c || !seq || !info) return PPC_ERR_INVALID_ARG;
   if (!c->err_host) { *seq = *info = 0; return PPC_OK; }
-  const volatile ErrWord* e = c->err_host;
+  const volatile ErrHost* e = c->err_host;
   *seq = e->seq;
   *info = e->info;
   return (ppc_status_t)e->code;
@@ -955,7 +969,7 @@ ppc_status_t ppc_error_info(ppc_comm_t* c, unsigned* seq, unsigned* info) {
 ppc_status_t ppc_poll(ppc_comm_t* c) {
   if (!c) return PPC_ERR_INVALID_ARG;
   if (!c->err_host) return PPC_OK;
-  const unsigned code = ((volatile ErrWord*)c->err_host)->code;
+  const unsigned code = ((volatile ErrHost*)c->err_host)->code;
   if (code) c->poisoned = true;
   return (ppc_status_t)code;
 }
@@ -1061,6 +1075,7 @@ ppc_status_t ppc_destroy(ppc_comm_t* c) {
     for (int d = 0; d < 2; ++d) if (c->zc_ev[d]) cudaEventDestroy(c->zc_ev[d]);
     if (c->arena) cudaFree(c->arena);
     if (c->err_host) cudaFreeHost(c->err_host);
+    if (c->err_dev) cudaFree(c->err_dev);
   }
   delete c;
   return PPC_OK;

@@ -144,10 +144,12 @@ struct ppc_comm {
   unsigned long long timeout_ns = 10000000000ull;
   Layout lay;
   uint8_t* arena = nullptr;
-  ErrWord* err_host = nullptr;
-  ErrWord* err_dev = nullptr;
+  ErrHost* err_host = nullptr;     // mapped host record (polled by the host)
+  ErrWord* err_dev = nullptr;      // device claim word + the record's device pointer
   bool connected = false, poisoned = false, local_mode = false;
   bool sys_scope = true;   // a PP neighbour is another GPU: .sys fences, NVLink-sized grids
+  int spin_cap = 64;       // max CTAs of a spinning grid (8 when a peer shares our GPU in
+                           // this process: cfg.local_spin, every stage must stay resident)
   Chan ch[2];
   std::vector<void*> opened;          // IPC-opened peer arenas
   ncclComm_t nccl[2] = {nullptr, nullptr};
@@ -245,7 +247,7 @@ inline uint64_t host_hash() {
 inline ppc_status_t check_live(ppc_comm* c) {
   if (!c || !c->connected) return PPC_ERR_STATE;
   if (c->poisoned) return PPC_ERR_STATE;
-  if (c->err_host && ((volatile ErrWord*)c->err_host)->code != 0) {
+  if (c->err_host && ((volatile ErrHost*)c->err_host)->code != 0) {
     c->poisoned = true;
     return PPC_ERR_STATE;
   }
@@ -278,9 +280,10 @@ inline int push_grid(const ppc_comm* c, uint32_t n_chunks) {
   if (n_chunks == 0) return 1;
   int per = c->cfg.cta_per_channel;
   int chans = std::max(1, c->cfg.channels);
-  int g = per > 0 ? per * chans : (c->sys_scope ? 64 * chans : 296);
+  int g = per > 0 ? per * chans : (c->sys_scope ? c->spin_cap * chans : 296);
   if (c->cfg.engine == PPC_ENGINE_PULL && c->sys_scope)
     g = env_int("PPC_STAGE_CTAS", 128);          // local staging copy: HBM-bound, wide
+  if (c->sys_scope) g = std::min(g, c->spin_cap * chans);
   return (int)std::max<uint32_t>(1, std::min<uint32_t>(n_chunks, (uint32_t)g));
 }
 // Receive-side grid: copy-out CTAs (SM/CE) or pulling CTAs (PULL).
@@ -290,6 +293,7 @@ inline int recv_grid(const ppc_comm* c, uint32_t n_chunks) {
   if (c->cfg.engine == PPC_ENGINE_PULL && c->sys_scope && c->cfg.cta_per_channel > 0)
     g = c->cfg.cta_per_channel * std::max(1, c->cfg.channels);      // the pulling CTAs
   g = env_int("PPC_RECV_CTAS", g);
+  if (c->sys_scope) g = std::min(g, c->spin_cap);
   return (int)std::max<uint32_t>(1, std::min<uint32_t>(n_chunks, (uint32_t)g));
 }
 

@@ -20,6 +20,7 @@ struct ppc_graph {
   std::vector<cudaEvent_t> captured;              // events referenced by the graph's nodes
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
+  unsigned long long kernels = 0;                 // libppc kernel nodes (ppc_launch_count)
 };
 
 namespace {
@@ -142,6 +143,7 @@ ppc_status_t ppc_graph_create(ppc_comm_t* const* comms, int n, const ppc_step_t*
   };
   DeviceGuard dg0(comms[0]->device);
   cudaStream_t s0 = g->cap[0];
+  const unsigned long long launches0 = g_launches.load();
   cudaError_t e = cudaStreamBeginCapture(s0, cudaStreamCaptureModeRelaxed);
   if (e != cudaSuccess) {
     GDBG("ppc: graph begin capture %s\n", cudaGetErrorString(e));
@@ -170,6 +172,8 @@ ppc_status_t ppc_graph_create(ppc_comm_t* const* comms, int n, const ppc_step_t*
   if (fork) cudaEventDestroy(fork);
   for (cudaEvent_t j : joins) if (j) cudaEventDestroy(j);
   st = finish(st);
+  g->kernels = g_launches.load() - launches0;   // captured, not run: counted per replay
+  g_launches.fetch_sub(g->kernels);
   g->graph = graph;
   if (!st) {
     e = cudaGraphInstantiate(&g->exec, graph, 0);
@@ -211,6 +215,7 @@ ppc_status_t ppc_graph_launch(ppc_graph_t* g) {
   {
     DeviceGuard d0(g->comms[0]->device);
     CK(cudaGraphLaunch(g->exec, g->cap[0]));
+    g_launches.fetch_add(g->kernels);
     CK(cudaEventRecord(g->ev_out, g->cap[0]));
   }
   for (int k = 0; k < n; ++k) {                 // the caller's streams continue after it

@@ -1,5 +1,6 @@
 // Internal declarations of libppc (not part of the C ABI).
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 #include "ppc.h"
@@ -31,9 +32,18 @@ struct __align__(64) SlotHeader {
 };
 static_assert(sizeof(SlotHeader) == 64, "slot header is 64 B");
 
-// Error word in mapped host memory: [0] = status code, [1] = seq, [2] = dir | kind << 8.
+// Sticky error record in mapped host memory (the host polls it without synchronising):
+// code = status, seq = message seq, info = where (see ppc_error_info).
+struct ErrHost {
+  unsigned code, seq, info, pad;
+};
+// What the kernels get: a claim word in DEVICE memory plus the mapped host record.  The first
+// failing thread wins the claim (atomicCAS; every kernel that latches into a comm's record
+// runs on that comm's device), then writes seq and info and, after a system fence, code —
+// so the record is never torn and the host never sees a code without its seq / info.
 struct ErrWord {
-  unsigned int code, seq, info, pad;
+  unsigned claim, pad;
+  ErrHost* host;      // device pointer of the mapped host record
 };
 
 // Graph-capturable sequence numbers.  base == nullptr: `seq` in the kernel args is absolute
@@ -174,6 +184,7 @@ cudaError_t preload_kernels();
 // PPC_PDL by ppc_create
 extern int g_pdl;
 extern int g_copy_tma_ctas;
+extern std::atomic<unsigned long long> g_launches;   // ppc_launch_count
 // wait until *credit >= target (+ *seq_base when seq_base != nullptr: graph replay)
 cudaError_t launch_wait_credit(const uint64_t* credit, uint64_t target, ErrWord* err,
                                uint64_t timeout_ns, cudaStream_t s,

@@ -11,6 +11,7 @@
 // Flags and credits are monotone u64 sequence numbers (never reset); every wait compares
 // wrap-safe and is bounded by %globaltimer (§4.3 P:L211 hangs).
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -19,6 +20,9 @@
 
 namespace ppc {
 
+// kernels this process enqueued through libppc (ppc_launch_count): every launch site bumps it;
+// a graph capture's launches are moved from it into the graph, which adds them per replay
+std::atomic<unsigned long long> g_launches{0};
 int g_pdl = 1;   // programmatic dependent launch for transport kernels (PPC_PDL, ppc_create)
 int g_recv_early = 0;   // receive looks for its publication before griddepcontrol.wait (PPC_RECV_EARLY)
 int g_copy_tma_ctas = 0;   // virtual-stage copy: TMA bulk grid; 0 = SIMT copy_kernel (PPC_COPY_TMA_CTAS)
@@ -94,6 +98,7 @@ cudaError_t launch_k(void (*k)(KArgs...), unsigned grid, unsigned block, cudaStr
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = (g_pdl && pdl) ? 1 : 0;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
@@ -165,8 +170,10 @@ __device__ __forceinline__ void st_data(uint4* p, const uint4& v) {
 }
 
 __device__ __forceinline__ void latch(ErrWord* e, unsigned code, uint64_t seq, unsigned info) {
-  // plain system-scope stores into mapped host memory; any error poisons the comm
-  volatile ErrWord* v = e;
+  // first failure wins (ErrWord): claim in device memory, then the mapped host record with
+  // its code stored last; any error poisons the comm
+  if (atomicCAS(&e->claim, 0u, 1u) != 0u) return;
+  volatile ErrHost* v = e->host;
   v->seq = (unsigned)seq;
   v->info = info;
   __threadfence_system();
@@ -567,7 +574,7 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(const __grid_constant__ 
         (((uintptr_t)(a0.dst + off) | (uintptr_t)(s_early_src + off)) & 31) == 0) {
       const V32* src = reinterpret_cast<const V32*>(s_early_src + off);
 #pragma unroll
-      for (int j = 0; j < kEarlyV; ++j) pre[j] = ld_src(src + threadIdx.x + j * kThreads);
+      for (int j = 0; j < kEarlyV; ++j) pre[j] = ld_ring(src + threadIdx.x + j * kThreads);
       pre_ok = true;
     }
   }
@@ -787,6 +794,7 @@ __global__ void set_seq_kernel(uint64_t* seq, uint64_t v0, uint64_t v1, uint64_t
 
 cudaError_t launch_set_seq(uint64_t* seq, uint64_t v0, uint64_t v1, uint64_t v2, uint64_t v3,
                            cudaStream_t s) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   set_seq_kernel<<<1, 1, 0, s>>>(seq, v0, v1, v2, v3);
   return cudaGetLastError();
 }
@@ -801,6 +809,7 @@ __global__ void add_kernel(T* __restrict__ dst, const T* __restrict__ src, size_
 cudaError_t launch_add(void* dst, const void* src, size_t count, int dtype, cudaStream_t s) {
   if (count == 0) return cudaSuccess;
   const int grid = (int)std::min<size_t>((count + 255) / 256, 148 * 8);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   switch (dtype) {
     case 0: add_kernel<float><<<grid, 256, 0, s>>>((float*)dst, (const float*)src, count); break;
     case 1: add_kernel<__half><<<grid, 256, 0, s>>>((__half*)dst, (const __half*)src, count); break;
@@ -937,6 +946,7 @@ cudaError_t launch_copy(void* dst, const void* src, uint64_t bytes, uint64_t chu
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = g_pdl ? 1 : 0;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     return cudaLaunchKernelEx(&cfg, copy_tma_kernel, static_cast<uint8_t*>(dst),
                               static_cast<const uint8_t*>(src), bytes);
   }
@@ -1129,6 +1139,7 @@ extern "C" ppc_status_t ppc_fill_payload(void* buf, size_t bytes, int seed, int 
     return PPC_ERR_INVALID_ARG;
   const uint64_t nw = (bytes + 7) / 8;
   const int grid = (int)std::min<uint64_t>((nw + 255) / 256, 148ull * 8);
+  ppc::g_launches.fetch_add(1, std::memory_order_relaxed);
   ppc::splitmix_xor_kernel<<<grid, 256, 0, s>>>(static_cast<uint8_t*>(buf), nullptr, bytes,
                                                ppc::payload_key(seed, step, boundary, dir, mb));
   return cudaGetLastError() == cudaSuccess ? PPC_OK : PPC_ERR_CUDA;
@@ -1141,8 +1152,13 @@ extern "C" int ppc_stage_xor(void* user, int mb, const void* in, void* out, size
   if (out_bytes == 0) return PPC_OK;
   const uint64_t nw = (out_bytes + 7) / 8;
   const int grid = (int)std::min<uint64_t>((nw + 255) / 256, 148ull * 8);
+  ppc::g_launches.fetch_add(1, std::memory_order_relaxed);
   ppc::splitmix_xor_kernel<<<grid, 256, 0, s>>>(
       static_cast<uint8_t*>(out), static_cast<const uint8_t*>(in), out_bytes,
       ppc::payload_key(c->seed ^ 0x8000, c->step, c->stage, c->dir, mb));
   return cudaGetLastError() == cudaSuccess ? PPC_OK : PPC_ERR_CUDA;
+}
+
+extern "C" unsigned long long ppc_launch_count(void) {
+  return ppc::g_launches.load(std::memory_order_relaxed);
 }

@@ -50,7 +50,9 @@ ppc_status_t ensure_bufs(ppc_comm* c, size_t bytes) {
     }
   }
   if (bytes <= sb.bytes) return PPC_OK;
-  CK(cudaDeviceSynchronize());
+  // only freeing old scratch needs the device idle (the first call allocates nothing that is
+  // in use; with cfg.local_spin another stage of this process may already be spinning)
+  if (!sb.in_arena && sb.rbuf[0][0]) CK(cudaDeviceSynchronize());
   // messages up to max_msg_bytes: the arena's step region (zeroed at create; a peer can
   // pull a forwarded message from it, zero-copy); larger scratch falls back to cudaMalloc
   const bool arena = c->arena && bytes <= c->lay.stride;

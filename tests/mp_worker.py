@@ -17,6 +17,13 @@ from oracle.proxy import xor_closed_form  # noqa: E402
 from synth import payload as P  # noqa: E402
 
 
+def dev(rank):
+    """CUDA device of a rank: its own GPU, or (fewer GPUs than ranks, e.g. the 1-GPU driver
+    box) GPUs shared round-robin — ranks on one GPU are separate processes, so CUDA IPC,
+    device spins and the per-rank step driver run exactly as across GPUs (time-sliced)."""
+    return rank % torch.cuda.device_count()
+
+
 def host(t):
     torch.cuda.synchronize()
     return t.cpu().numpy().view(np.uint8).reshape(-1)
@@ -29,7 +36,7 @@ def buf(n):
 def case_sendrecv(rank, world, engine):
     cfg = ppc.make_config(pp=world, max_msg_bytes=8 << 20, chunk_bytes=256 << 10, engine=engine,
                           channels=4 if engine else 1)
-    comm = ppc.connect_distributed(cfg, rank, world, rank, with_nccl=False)
+    comm = ppc.connect_distributed(cfg, rank, world, dev(rank), with_nccl=False)
     s = torch.cuda.current_stream()
     sizes = [0, 1, 4096, 3 * (256 << 10) + 5, 8 << 20]
     for rep in range(3):
@@ -59,7 +66,7 @@ def case_xor(rank, world, engine, M=6):
     n = 5 * (256 << 10) + 777
     cfg = ppc.make_config(pp=S, max_msg_bytes=n, chunk_bytes=256 << 10, engine=engine,
                           channels=2 if engine else 1, trace=1)
-    comm = ppc.connect_distributed(cfg, rank, world, rank, with_nccl=False)
+    comm = ppc.connect_distributed(cfg, rank, world, dev(rank), with_nccl=False)
     X = [buf(n) for _ in range(M)] if rank == 0 else None
     G = [buf(n) for _ in range(M)] if rank == S - 1 else None
     out = [buf(n) for _ in range(M)]
@@ -99,7 +106,7 @@ def case_host(rank, world, M=6):
     S = world
     n = 3 * (256 << 10) + 321
     cfg = ppc.make_config(pp=S, max_msg_bytes=n, chunk_bytes=256 << 10)
-    comm = ppc.connect_distributed(cfg, rank, world, rank, with_nccl=False)
+    comm = ppc.connect_distributed(cfg, rank, world, dev(rank), with_nccl=False)
     pin = lambda a: torch.from_numpy(a.copy()).pin_memory()
     hX = [pin(P.source_activation(42, 0, m, n)) for m in range(M)] if rank == 0 else None
     hG = [pin(P.source_gradient(42, 0, m, n)) for m in range(M)] if rank == S - 1 else None
@@ -133,7 +140,7 @@ def case_host(rank, world, M=6):
 
 def case_timeout(rank, world):
     cfg = ppc.make_config(pp=world, max_msg_bytes=1 << 20, timeout_ns=300_000_000)
-    comm = ppc.connect_distributed(cfg, rank, world, rank, with_nccl=False)
+    comm = ppc.connect_distributed(cfg, rank, world, dev(rank), with_nccl=False)
     if rank == 1:
         b = buf(4096)
         comm.recv(ppc.FWD, b, 4096, mb=0, stream=torch.cuda.current_stream())
@@ -146,7 +153,7 @@ def case_dcbs(rank, world):
     """PP=2 x TP=2 on 4 GPUs: TP allreduce on NCCL running beside the PP kernels."""
     tp = 2
     cfg = ppc.make_config(tp=tp, pp=world // tp, dp=1, max_msg_bytes=1 << 20)
-    comm = ppc.connect_distributed(cfg, rank, world, rank, with_nccl=True)
+    comm = ppc.connect_distributed(cfg, rank, world, dev(rank), with_nccl=True)
     tp_m, be = comm.group(ppc.GROUP_TP)
     pp_m, be2 = comm.group(ppc.GROUP_PP)
     assert be == ppc.BACKEND_NCCL and be2 == ppc.BACKEND_PEER and len(tp_m) == tp
@@ -194,7 +201,7 @@ def case_toy(rank, world, bf16=True, steps=5):
     st = ToyStage(rank, ROWS, WIDTH, M, 10.0, bf16, rank, Ws[2 * rank:2 * rank + 2],
                   bs[2 * rank:2 * rank + 2], X if rank == 0 else T)
     cfg = ppc.make_config(pp=2, max_msg_bytes=st.boundary_bytes, chunk_bytes=64 << 10)
-    comm = ppc.connect_distributed(cfg, rank, world, rank, with_nccl=False)
+    comm = ppc.connect_distributed(cfg, rank, world, dev(rank), with_nccl=False)
     s = torch.cuda.current_stream()
     args = st.step_args()
     losses = []
@@ -218,7 +225,7 @@ def case_zc(rank, world):
     """Zero-copy pulls from registered send buffers: ragged sizes byte-exact, then an identity
     1F1B step whose X / G sources are registered (the receiver pulls them over NVLink)."""
     cfg = ppc.make_config(pp=world, max_msg_bytes=8 << 20, chunk_bytes=256 << 10)
-    comm = ppc.connect_distributed(cfg, rank, world, rank, with_nccl=False)
+    comm = ppc.connect_distributed(cfg, rank, world, dev(rank), with_nccl=False)
     s = torch.cuda.current_stream()
     sizes = [1, 4096 + 3, 3 * (256 << 10) + 5, 8 << 20]
     src = [buf(n) for n in sizes]
@@ -269,7 +276,7 @@ def case_zc_bidir_stream(rank, world):
     n, N = 32 << 20, 8
     cfg = ppc.make_config(pp=world, max_msg_bytes=n, chunk_bytes=128 << 10,
                           timeout_ns=5_000_000_000)      # 256 chunks: grids up to 256 CTAs
-    comm = ppc.connect_distributed(cfg, rank, world, rank, with_nccl=False)
+    comm = ppc.connect_distributed(cfg, rank, world, dev(rank), with_nccl=False)
     src = buf(n)
     ppc.fill_payload(src, n, 42, 0, 0, rank, 0)
     ppc.register_tensors(comm, [src])
@@ -300,7 +307,7 @@ def case_zc_async(rank, world):
     directions at once, ragged sizes; every message byte-exact and in order."""
     sizes = [1, 4096 + 3, 3 * (256 << 10) + 5, 8 << 20, 5 << 20]
     cfg = ppc.make_config(pp=world, max_msg_bytes=8 << 20, chunk_bytes=256 << 10, zc_async=1)
-    comm = ppc.connect_distributed(cfg, rank, world, rank, with_nccl=False)
+    comm = ppc.connect_distributed(cfg, rank, world, dev(rank), with_nccl=False)
     src = [buf(n) for n in sizes]
     for i, (b, n) in enumerate(zip(src, sizes)):
         ppc.fill_payload(b, n, 42, 0, 0, rank, i)
@@ -331,7 +338,7 @@ def case_graph(rank, world, zc=False):
     are registered (zero-copy pulls inside the graph)."""
     S, M, n = world, 4, 3 * (256 << 10) + 99
     cfg = ppc.make_config(pp=S, max_msg_bytes=n, chunk_bytes=256 << 10)
-    comm = ppc.connect_distributed(cfg, rank, world, rank, with_nccl=False)
+    comm = ppc.connect_distributed(cfg, rank, world, dev(rank), with_nccl=False)
     s = torch.cuda.current_stream()
     X = [buf(n) for _ in range(M)] if rank == 0 else None
     G = [buf(n) for _ in range(M)] if rank == S - 1 else None
@@ -399,7 +406,7 @@ def case_fullsize(rank, world):
     hidden, M = (4096, 8) if world == 2 else (3584, 32)
     n = 4096 * hidden * 2
     cfg = ppc.make_config(pp=S, max_msg_bytes=n, chunk_bytes=256 << 10)
-    comm = ppc.connect_distributed(cfg, rank, world, rank, with_nccl=False)
+    comm = ppc.connect_distributed(cfg, rank, world, dev(rank), with_nccl=False)
     s = torch.cuda.Stream()
     X = [buf(n) for _ in range(M)] if rank == 0 else None
     G = [buf(n) for _ in range(M)] if rank == S - 1 else None
@@ -436,7 +443,7 @@ def case_gather(rank, world):
     from oracle.collectives import tp_gather_reference
     tp = 2
     cfg = ppc.make_config(tp=tp, pp=world // tp, dp=1, max_msg_bytes=4 << 20, chunk_bytes=256 << 10)
-    comm = ppc.connect_distributed(cfg, rank, world, rank, with_nccl=False)
+    comm = ppc.connect_distributed(cfg, rank, world, dev(rank), with_nccl=False)
     s = torch.cuda.current_stream()
     pp_i, tp_i = rank // tp, rank % tp
     slice_n = 3 * (256 << 10) + 77
@@ -472,7 +479,7 @@ def case_hetero(rank, world):
     dp = 2 if world >= 4 else 1
     pp = world // dp
     cfg = ppc.make_config(tp=1, pp=pp, dp=dp, max_msg_bytes=8 << 20)
-    comm = ppc.connect_distributed(cfg, rank, world, rank, with_nccl=True)
+    comm = ppc.connect_distributed(cfg, rank, world, dev(rank), with_nccl=True)
     n = (1 << 20) + 3
     idx = np.arange(n, dtype=np.int64)
     vals = {r: ((r + 1) * (idx % 7 + 1)).astype(np.float32) for r in range(world)}
@@ -494,7 +501,7 @@ def case_inplace(rank, world, M=6):
     import ctypes as C
     S, n = world, 5 * (256 << 10) + 777
     cfg = ppc.make_config(pp=S, max_msg_bytes=n, chunk_bytes=256 << 10)
-    comm = ppc.connect_distributed(cfg, rank, world, rank, with_nccl=False)
+    comm = ppc.connect_distributed(cfg, rank, world, dev(rank), with_nccl=False)
     s = torch.cuda.current_stream()
     xor = ppc._lib.ppc_stage_xor
     xor.restype = C.c_int
@@ -536,7 +543,7 @@ def main():
     case = sys.argv[1]
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
-    torch.cuda.set_device(rank)
+    torch.cuda.set_device(dev(rank))
     dist.init_process_group("gloo")
     if case == "sendrecv_sm":
         comm = case_sendrecv(rank, world, ppc.ENGINE_SM)
