@@ -35,8 +35,9 @@ def parse():
     ap.add_argument("--sm", default="16:1M,32:1M,64:1M,32:256K,64:256K,128:256K,32:4M")
     ap.add_argument("--ce", default="1,2,4,8")
     ap.add_argument("--pull", default="", help="PULL engine specs cta:chunk, e.g. 32:1M,64:1M")
-    ap.add_argument("--zc", default="", help="zero-copy specs recv_ctas:chunk[:a], e.g. 64:256K "
-                                             "(:a = cfg.zc_async, sends complete at publication)")
+    ap.add_argument("--zc", default="", help="zero-copy specs recv_ctas:chunk[:flags], e.g. "
+                                             "64:256K:ab (a = cfg.zc_async, sends complete at "
+                                             "publication; b = batched receives, 16 per grid)")
     ap.add_argument("--modes", default="uni,bidir")
     ap.add_argument("--comparators", default="nccl,ce_copy,gloo")
     ap.add_argument("--reps", type=int, default=5)
@@ -57,7 +58,7 @@ def emit(fh, rec):
     fh.flush()
 
 
-def bench_ppc(comm, rank, sizes, modes, label, reps, fh, zc=False):
+def bench_ppc(comm, rank, sizes, modes, label, reps, fh, zc=False, batch=0):
     s_send = torch.cuda.Stream()
     s_recv = torch.cuda.Stream()
     maxn = max(sizes)
@@ -78,7 +79,14 @@ def bench_ppc(comm, rank, sizes, modes, label, reps, fh, zc=False):
                 torch.cuda.synchronize()
                 dist.barrier()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                if receiver:
+                if receiver and batch:       # ppc_pp_recv_batch: `batch` messages per grid
+                    k0 = min(batch, N)           # distinct destinations inside one grid
+                    dsts = [dst] + [torch.empty(n, dtype=torch.uint8, device="cuda")
+                                    for _ in range(k0 - 1)]
+                    for i0 in range(0, N, batch):
+                        k = min(batch, N - i0)
+                        comm.recv_batch(d_in, dsts[:k], n, mb0=i0, stream=s_recv)
+                elif receiver:
                     for i in range(N):
                         comm.recv(d_in, dst, n, mb=i, stream=s_recv)
                 if sender:
@@ -209,16 +217,18 @@ def main():
         dist.barrier()
         comm.destroy()
     for spec in [x for x in a.zc.split(",") if x]:
-        parts = spec.split(":")            # recv_ctas:chunk[:a]  (a = cfg.zc_async)
+        parts = spec.split(":")            # recv_ctas:chunk[:flags]  (a = zc_async, b = batch)
         rc, chunk = parts[0], parts[1]
-        zc_async = len(parts) > 2 and parts[2] == "a"
+        zc_async = len(parts) > 2 and "a" in parts[2]
+        batch = 16 if len(parts) > 2 and "b" in parts[2] else 0
         os.environ["PPC_RECV_CTAS"] = rc
         cfg = ppc.make_config(pp=world, max_msg_bytes=maxn, chunk_bytes=size_of(chunk),
                               zc_async=int(zc_async))
         comm = ppc.connect_distributed(cfg, rank, world, torch.cuda.current_device(),
                                        with_nccl=False)
-        label = f"ppc_zerocopy{'_async' if zc_async else ''}_recv{rc}_chunk{chunk}"
-        bench_ppc(comm, rank, sizes, modes, label, a.reps, fh, zc=True)
+        label = (f"ppc_zerocopy{'_async' if zc_async else ''}{'_batch' if batch else ''}"
+                 f"_recv{rc}_chunk{chunk}")
+        bench_ppc(comm, rank, sizes, modes, label, a.reps, fh, zc=True, batch=batch)
         os.environ.pop("PPC_RECV_CTAS")
         dist.barrier()
         comm.disconnect()

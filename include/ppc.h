@@ -251,6 +251,17 @@ ppc_status_t ppc_register(ppc_comm_t* c, const void* ptr, size_t bytes, void* bl
                           size_t* blob_bytes);
 ppc_status_t ppc_register_import(ppc_comm_t* c, const void* blob, size_t blob_bytes);
 
+/* Batched receive: the next n (1..16) messages of direction d into bufs[i] (bytes[i] each,
+ * micro-batch mb0 + i), exactly as n consecutive ppc_pp_recv calls — but in ONE grid whose
+ * CTAs move on to message i+1 as soon as their share of message i is done, so consecutive
+ * messages overlap their ramp and tail instead of paying a kernel boundary each (a stream
+ * of messages: the C5 sweep, a stage receiving several micro-batches back to back).  Credits
+ * are returned per message, in order; the n buffers must not overlap (CTAs of one grid may
+ * write messages i and i+1 at the same time).  Errors as ppc_pp_recv (per message).  In the
+ * virtual-stage mode all n sends must already be enqueued (else PPC_ERR_WOULD_BLOCK). */
+ppc_status_t ppc_pp_recv_batch(ppc_comm_t* c, ppc_dir_t d, void* const* bufs,
+                               const size_t* bytes, int n, long long mb0, cudaStream_t s);
+
 /* TP-sliced boundary with a fused all-gather (BJ configs[2], PP x TP):
  * every TP rank of the sending stage sends only its 1/TP slice (ppc_pp_send of slice bytes
  * from a REGISTERED buffer); every TP rank of the receiving stage calls ppc_pp_recv_gather

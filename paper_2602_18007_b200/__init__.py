@@ -108,6 +108,7 @@ _step = _sig("ppc_step_1f1b", _i, [_vp, C.POINTER(Step), _vp])
 _step_local = _sig("ppc_step_1f1b_local", _i, [C.POINTER(_vp), _i, C.POINTER(Step), C.POINTER(_vp)])
 _allreduce = _sig("ppc_allreduce", _i, [_vp, _i, _vp, _sz, _i, _vp])
 _hx_allreduce = _sig("ppc_hetero_allreduce", _i, [_vp, _vp, _sz, _i, _vp])
+_recv_batch = _sig("ppc_pp_recv_batch", _i, [_vp, _i, C.POINTER(_vp), C.POINTER(_sz), _i, _ll, _vp])
 _recv_gather = _sig("ppc_pp_recv_gather", _i, [_vp, _i, _vp, _sz, _ll, _vp])
 _graph_create = _sig("ppc_graph_create", _i, [C.POINTER(_vp), _i, C.POINTER(Step), C.POINTER(_vp),
                                               C.POINTER(_vp)])
@@ -267,6 +268,16 @@ class Comm:
         p, n = _ptr(tensor)
         _check(_allreduce(self.h, g, p, tensor.numel(), nccl_dtype, _stream(stream)),
                "ppc_allreduce")
+
+    def recv_batch(self, direction, bufs, nbytes, mb0=0, stream=None):
+        """The next len(bufs) messages of `direction` in one grid (ppc_pp_recv_batch);
+        nbytes: one size for all, or a list."""
+        n = len(bufs)
+        sizes = list(nbytes) if isinstance(nbytes, (list, tuple)) else [nbytes] * n
+        ps = (C.c_void_p * n)(*[_ptr(b)[0] for b in bufs])
+        ss = (C.c_size_t * n)(*sizes)
+        _check(_recv_batch(self.h, direction, ps, ss, n, mb0, _stream(stream)),
+               "ppc_pp_recv_batch")
 
     def recv_gather(self, direction, buf, nbytes=None, mb=0, stream=None):
         """TP-sliced boundary: receive every TP sender's slice (pulled, fused all-gather)."""

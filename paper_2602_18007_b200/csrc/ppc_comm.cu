@@ -752,6 +752,81 @@ ppc_status_t ppc_impl_recv_ex(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t byte
   return PPC_OK;
 }
 
+ppc_status_t ppc_pp_recv_batch(ppc_comm_t* c, ppc_dir_t d, void* const* bufs,
+                               const size_t* bytes, int n, long long mb0, cudaStream_t s) {
+  ppc_status_t st = check_live(c);
+  if (st) return st;
+  if (d != PPC_FWD && d != PPC_BWD) return PPC_ERR_INVALID_ARG;
+  if (n < 1 || n > kMaxBatch || !bufs || !bytes || mb0 < 0) return PPC_ERR_INVALID_ARG;
+  Chan& h = c->ch[d];
+  if (h.peer_in < 0) return PPC_ERR_NO_NEIGHBOR;
+  if (c->device < 0) return PPC_ERR_STATE;
+  uint32_t max_chunks = 1;
+  for (int i = 0; i < n; ++i) {
+    if (bytes[i] > 0 && !bufs[i]) return PPC_ERR_INVALID_ARG;
+    if (bytes[i] > c->cfg.max_msg_bytes) return PPC_ERR_TOO_LARGE;
+    max_chunks = std::max<uint32_t>(max_chunks, (uint32_t)((bytes[i] + c->chunk - 1) / c->chunk));
+  }
+  DeviceGuard g(c->device);
+  if (c->local_mode) {                   // virtual stages: every message's send enqueued
+    Chan& sh = h.in_comm->ch[d];
+    if (sh.send_seq < h.recv_seq + n) return PPC_ERR_WOULD_BLOCK;
+    for (int i = 0; i < n; ++i) {
+      const uint64_t seq = h.recv_seq + 1 + i;
+      if (!(c->capturing && seq <= h.in_comm->cap_send[d]))
+        CK(cudaStreamWaitEvent(s, sh.sent_ev[seq % c->K], 0));
+    }
+  }
+  static thread_local RecvBatch b;       // ~8 KiB: kept off the stack
+  memset(&b, 0, sizeof(b));
+  b.n = (uint32_t)n;
+  for (int i = 0; i < n; ++i) {
+    const uint64_t seq = h.recv_seq + 1 + i;
+    const int slot = (int)(seq % c->K);
+    RecvArgs& a = b.a[i];
+    a.dst = static_cast<uint8_t*>(bufs[i]);
+    a.src = h.i_payload + (size_t)slot * c->lay.stride;
+    a.hdr = h.i_hdr + slot;
+    a.hdr_flag = h.i_hdr_flag + slot;
+    a.flags = h.i_flags + (size_t)slot * std::max<uint32_t>(c->lay.max_chunks, 1);
+    a.peer_credit = h.peer_credit;
+    a.done = h.i_done + slot;
+    a.bytes = bytes[i];
+    a.chunk = c->chunk;
+    a.n_chunks = (uint32_t)((bytes[i] + c->chunk - 1) / c->chunk);
+    a.seq = seq;
+    a.mb = mb0 + i;
+    a.err = c->err_dev;
+    a.timeout_ns = c->timeout_ns;
+    a.rec = next_record(c);
+    a.rec_src = h.peer_in;
+    a.rec_dst = c->rank;
+    a.seg_tab = c->seg_tab
+        ? c->seg_tab + ((size_t)(d == PPC_FWD ? 0 : 1) * c->cfg.tp + c->tp_i) * kMaxSeg : nullptr;
+    a.peer_arena = h.i_arena;
+    if (c->capturing) {                  // graph: relative seq, slot resolved on device
+      a.sr = {c->dseq + 2 + d, (uint64_t)c->lay.stride, (uint32_t)c->K,
+              std::max<uint32_t>(c->lay.max_chunks, 1), 0, 0};
+      a.seq = seq - c->cap_recv[d];
+      a.src = h.i_payload;
+      a.hdr = h.i_hdr;
+      a.hdr_flag = h.i_hdr_flag;
+      a.flags = h.i_flags;
+      a.done = h.i_done;
+    }
+  }
+  if (ppc_status_t ts = time_mark(c, 1, s, true)) return ts;
+  CK(launch_recv_batch(b, recv_grid(c, max_chunks), c->sys_scope, s));
+  if (ppc_status_t ts = time_mark(c, 1, s, false)) return ts;
+  h.recv_seq += (uint64_t)n;
+  if (c->local_mode)
+    for (int i = 0; i < n; ++i) {
+      const uint64_t seq = h.recv_seq - n + 1 + i;
+      CK(cudaEventRecord(h.recvd_ev[seq % c->K], s));
+    }
+  return PPC_OK;
+}
+
 ppc_status_t ppc_pp_recv_gather(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t total_bytes,
                                 long long mb, cudaStream_t s) {
   ppc_status_t st = check_live(c);

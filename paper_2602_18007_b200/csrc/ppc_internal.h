@@ -123,6 +123,15 @@ struct RecvArgs {
 extern int g_recv_early;
 cudaError_t launch_publish(const PublishArgs& a, cudaStream_t s);
 
+// ppc_pp_recv_batch: n consecutive receives of one direction in one grid (kernel parameter
+// space holds the descriptors: n x sizeof(RecvArgs) <= ~8 KiB).
+constexpr int kMaxBatch = 16;
+struct RecvBatch {
+  uint32_t n, pad;
+  RecvArgs a[kMaxBatch];
+};
+cudaError_t launch_recv_batch(const RecvBatch& b, int grid, bool sys, cudaStream_t s);
+
 // TP-sliced receive with a fused all-gather (ppc_pp_recv_gather).
 constexpr int kMaxTp = 8;
 struct GatherArgs {

@@ -11,6 +11,7 @@
 // Flags and credits are monotone u64 sequence numbers (never reset); every wait compares
 // wrap-safe and is bounded by %globaltimer (§4.3 P:L211 hangs).
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <cstdint>
 #include <cuda_bf16.h>
@@ -668,6 +669,94 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(const __grid_constant__ 
   }
 }
 
+// ---------------------------------------------------------------- K10b: batched receive
+// ppc_pp_recv_batch: ONE grid receives n consecutive messages of a direction.  Every CTA
+// walks the messages in order and moves on to message i+1 as soon as its own share of
+// message i is done, so the tail of one message overlaps the ramp of the next (no grid-wide
+// drain + relaunch per message, which costs several us at NVLink rates).  Per message the
+// protocol is recv_kernel's: thread 0 acquires the header flag (bounded), checks the header,
+// the CTA pulls its chunks (zero-copy) or copies them out behind the chunk flags (ring);
+// the CTA that completes the message's count releases its credit.  Credits leave in message
+// order without extra waiting: the last CTA of message i+1 counted itself after finishing
+// message i, which it did after its own arrival on i (fence + atomic chain), so credit i is
+// stored before credit i+1.
+template <bool kSys>
+__global__ void __launch_bounds__(kThreads) recv_batch_kernel(const __grid_constant__ RecvBatch b) {
+  __shared__ const uint8_t* s_zc_src;
+  pdl_enter();
+  for (uint32_t i = 0; i < b.n; ++i) {
+    const RecvArgs a = resolve(b.a[i]);
+    int fail = 0;
+    uint64_t deadline = 0;
+    if (threadIdx.x == 0) {
+      const uint64_t t0 = globaltimer();
+      deadline = t0 + a.timeout_ns;
+      s_zc_src = nullptr;
+      if (a.rec && blockIdx.x == 0)
+        fill_record(a.rec, (long long)t0, a.rec_src, a.rec_dst, -1, 1, a.seq, a.mb, a.bytes);
+      if (!wait_geq<kSys>(a.hdr_flag, a.seq, deadline)) {
+        latch(a.err, PPC_ERR_TIMEOUT, a.seq, 0x100u);
+        fail = 1;
+      } else {
+        const volatile SlotHeader* h = a.hdr;
+        if (h->magic != kMagic || h->seq != a.seq || h->mb != a.mb) {
+          latch(a.err, PPC_ERR_ORDER, a.seq, 0x100u);
+          fail = 1;
+        } else if (h->bytes != a.bytes) {
+          latch(a.err, PPC_ERR_SIZE_MISMATCH, a.seq, 0x100u);
+          fail = 1;
+        } else if (h->flags & kHdrZeroCopy) {
+          const uint64_t base = zc_base(a, h->src_seg);
+          if (!base) {
+            latch(a.err, PPC_ERR_ORDER, a.seq, 0x300u | h->src_seg << 12);
+            fail = 1;
+          } else {
+            s_zc_src = reinterpret_cast<const uint8_t*>(base + h->src_off);
+            if (a.rec && blockIdx.x == 0) a.rec->t_start_ns = (long long)globaltimer();
+          }
+        }
+      }
+    }
+    if (__syncthreads_or(fail)) return;
+    const uint8_t* zc_src = s_zc_src;
+    // rotate the chunk ownership per message so the CTAs that carried the last chunks of
+    // one message start the next one early
+    const uint32_t first = (blockIdx.x + i * (a.n_chunks % gridDim.x)) % gridDim.x;
+    for (uint32_t c = first; c < a.n_chunks; c += gridDim.x) {
+      const uint64_t off = (uint64_t)c * a.chunk;
+      const uint64_t len = min(a.chunk, a.bytes - off);
+      if (zc_src) {
+        cta_copy<true>(a.dst + off, zc_src + off, len);
+        continue;
+      }
+      int f = 0;
+      if (threadIdx.x == 0 && !wait_geq<kSys>(a.flags + c, a.seq, deadline)) {
+        latch(a.err, PPC_ERR_TIMEOUT, a.seq, 0x100u | c << 12);
+        f = 1;
+      }
+      if (__syncthreads_or(f)) return;
+      cta_copy<true>(a.dst + off, a.src + off, len);
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (atomicAdd(a.done, 1u) == gridDim.x - 1) {
+        *a.done = 0;
+        __threadfence();
+        st_rel<kSys>(a.peer_credit, a.seq);
+        if (a.rec) a.rec->t_end_ns = (long long)globaltimer();
+      }
+    }
+  }
+}
+
+cudaError_t launch_recv_batch(const RecvBatch& b, int grid, bool sys, cudaStream_t s) {
+  auto k = sys ? recv_batch_kernel<true> : recv_batch_kernel<false>;
+  if (sys) grid = std::min(grid, kMaxSpinGrid);
+  grid = fit_grid(k, grid, kThreads);
+  return launch_k(k, grid, kThreads, s, pdl_fits(k, grid, kThreads), b);
+}
+
 // ---------------------------------------------------------------- TP-sliced gather (NEXT-1)
 __global__ void __launch_bounds__(kThreads) gather_kernel(GatherArgs a) {
   pdl_enter();
@@ -995,10 +1084,10 @@ cudaError_t launch_ce_flags(uint64_t* flags, uint32_t c0, uint32_t c1, uint64_t 
 // spinning on a peer would then block the peer's first receive launch until the wait
 // times out.  Touching the functions up front (cudaFuncGetAttributes loads them) keeps
 // every later launch free of module loads.
-__global__ void __launch_bounds__(kThreads) xor_send_kernel(uint8_t* out, uint64_t* flags,
-                                                            uint64_t seq, const uint8_t* in,
-                                                            uint64_t bytes, uint64_t chunk,
-                                                            uint32_t n_chunks, uint64_t key);
+__global__ void __launch_bounds__(kWsThreads) xor_send_kernel(uint8_t* out, uint64_t* flags,
+                                                              uint64_t seq, const uint8_t* in,
+                                                              uint64_t bytes, uint64_t chunk,
+                                                              uint32_t n_chunks, uint64_t key);
 cudaError_t preload_kernels() {
   cudaFuncAttributes fa;
   const void* fns[] = {
@@ -1007,6 +1096,7 @@ cudaError_t preload_kernels() {
       (const void*)recv_kernel<true, false>, (const void*)recv_kernel<false, false>,
       (const void*)recv_kernel<true, false, true>, (const void*)recv_kernel<true, true, true>,
       (const void*)recv_kernel<true, true>,  (const void*)recv_kernel<false, true>,
+      (const void*)recv_batch_kernel<true>, (const void*)recv_batch_kernel<false>,
       (const void*)gather_kernel,          (const void*)publish_kernel,
       (const void*)ce_head_kernel,         (const void*)ce_flags_kernel,
       (const void*)wait_credit_kernel,     (const void*)set_seq_kernel,
@@ -1068,48 +1158,79 @@ __global__ void splitmix_xor_kernel(uint8_t* out, const uint8_t* in, uint64_t by
   }
 }
 
-// The XOR stage proxy fused with its send (ppc_stage_xor_send): CTA-per-chunk, the stage's
-// output goes straight into the receiver's slot (NVLink stores, 16 B per thread), then one
-// thread per CTA fences and releases that chunk's flag (the push kernel's protocol), so
-// the receiver copies chunk c out while later chunks are still being produced.
-__global__ void __launch_bounds__(kThreads) xor_send_kernel(uint8_t* out, uint64_t* flags,
-                                                            uint64_t seq, const uint8_t* in,
-                                                            uint64_t bytes, uint64_t chunk,
-                                                            uint32_t n_chunks, uint64_t key) {
+// The XOR stage proxy fused with its send (ppc_stage_xor_send): the stage's output goes
+// straight into the receiver's slot over NVLink, so the receiver copies chunk c out while
+// later chunks are still being produced.  Warp-specialised like push_ws_kernel: warps 1..16
+// compute out = in ^ stream and store it with 32-B vectors (st.global.v8, 4 stream words
+// per thread per step), chunk after chunk of the CTA's chunks; each finished chunk is handed
+// through an mbarrier ring to warp 0, which issues fence.acq_rel.sys + st.release.sys of
+// that chunk's flag while the copy warps already store the next chunk (r1: CTA per chunk,
+// 16-B stores, a CTA-wide barrier + fence before every flag: 537 GB/s).
+__global__ void __launch_bounds__(kWsThreads) xor_send_kernel(uint8_t* out, uint64_t* flags,
+                                                              uint64_t seq, const uint8_t* in,
+                                                              uint64_t bytes, uint64_t chunk,
+                                                              uint32_t n_chunks, uint64_t key) {
   pdl_enter();                     // the slot's credit wait (ce_head_kernel) has completed
+  __shared__ __align__(8) uint64_t full[kWsRing], empty[kWsRing];
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < kWsRing; ++b) {
+      mbar_init(&full[b], kWsCopyWarps);
+      mbar_init(&empty[b], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
   const uint64_t base = mix64(key + kGamma);
-  const bool vec = ((((uintptr_t)out) | ((uintptr_t)in)) & 15) == 0 && (chunk & 15) == 0;
-  for (uint32_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+  const bool vec = ((((uintptr_t)out) | ((uintptr_t)in)) & 31) == 0 && (chunk & 31) == 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t i = 0;
+  if (warp == 0) {                                   // signal warp
+    if (lane == 0) {
+      for (uint32_t c = blockIdx.x; c < n_chunks; c += gridDim.x, ++i) {
+        const int b = i % kWsRing;
+        mbar_wait(&full[b], (i / kWsRing) & 1);
+        fence_acq_rel_sys();
+        st_release_sys(flags + c, seq);
+        mbar_arrive(&empty[b]);
+      }
+    }
+    return;
+  }
+  const uint64_t tid = threadIdx.x - 32, nt = 32 * kWsCopyWarps;
+  for (uint32_t c = blockIdx.x; c < n_chunks; c += gridDim.x, ++i) {
+    const int b = i % kWsRing;
+    if (i >= kWsRing) mbar_wait(&empty[b], ((i / kWsRing) - 1) & 1);
     const uint64_t off = (uint64_t)c * chunk, end = min(off + chunk, bytes);
     uint64_t k = off;
-    if (vec) {                     // word pairs (w, w+1), w even, inside the chunk
-      const uint64_t np = (end - off) / 16;
-      for (uint64_t p = threadIdx.x; p < np; p += blockDim.x) {
-        const uint64_t w = off / 8 + 2 * p;
-        uint64_t v0 = mix64(base + (w + 1) * kGamma), v1 = mix64(base + (w + 2) * kGamma);
+    if (vec) {                     // 4-word quads (w .. w+3), w a multiple of 4, in the chunk
+      const uint64_t nq = (end - off) / 32;
+      for (uint64_t q = tid; q < nq; q += nt) {
+        const uint64_t w = off / 8 + 4 * q;
+        uint64_t v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = mix64(base + (w + 1 + j) * kGamma);
         if (in) {
-          const uint4 x = ld_src(reinterpret_cast<const uint4*>(in + 8 * w));
-          v0 ^= (uint64_t)x.x | (uint64_t)x.y << 32;
-          v1 ^= (uint64_t)x.z | (uint64_t)x.w << 32;
+          const V32 x = ld_src(reinterpret_cast<const V32*>(in + 8 * w));
+          v[0] ^= (uint64_t)x.lo.x | (uint64_t)x.lo.y << 32;
+          v[1] ^= (uint64_t)x.lo.z | (uint64_t)x.lo.w << 32;
+          v[2] ^= (uint64_t)x.hi.x | (uint64_t)x.hi.y << 32;
+          v[3] ^= (uint64_t)x.hi.z | (uint64_t)x.hi.w << 32;
         }
-        uint4 y;
-        y.x = (uint32_t)v0; y.y = (uint32_t)(v0 >> 32);
-        y.z = (uint32_t)v1; y.w = (uint32_t)(v1 >> 32);
-        st_data(reinterpret_cast<uint4*>(out + 8 * w), y);
+        V32 y;
+        y.lo = make_uint4((uint32_t)v[0], (uint32_t)(v[0] >> 32), (uint32_t)v[1], (uint32_t)(v[1] >> 32));
+        y.hi = make_uint4((uint32_t)v[2], (uint32_t)(v[2] >> 32), (uint32_t)v[3], (uint32_t)(v[3] >> 32));
+        st_data(reinterpret_cast<V32*>(out + 8 * w), y);
       }
-      k = off + np * 16;
+      k = off + nq * 32;
     }
-    for (uint64_t b = k + threadIdx.x; b < end; b += blockDim.x) {   // bytewise remainder
-      const uint64_t v = mix64(base + (b / 8 + 1) * kGamma);
-      uint8_t x = (uint8_t)(v >> (8 * (b & 7)));
-      if (in) x ^= in[b];
-      out[b] = x;
+    for (uint64_t bb = k + tid; bb < end; bb += nt) {   // bytewise remainder
+      const uint64_t v = mix64(base + (bb / 8 + 1) * kGamma);
+      uint8_t x = (uint8_t)(v >> (8 * (bb & 7)));
+      if (in) x ^= in[bb];
+      out[bb] = x;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      fence_acq_rel_sys();
-      st_release_sys(flags + c, seq);
-    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&full[b]);
   }
 }
 
@@ -1121,9 +1242,14 @@ extern "C" ppc_status_t ppc_stage_xor_send(const ppc_slot_t* slot, const ppc_xor
   if (!slot || !ctx || !slot->payload || !slot->flags || bytes == 0 || bytes != slot->bytes ||
       slot->chunk_bytes == 0 || slot->n_chunks != (bytes + slot->chunk_bytes - 1) / slot->chunk_bytes)
     return PPC_ERR_INVALID_ARG;
-  const int grid = (int)std::min<uint32_t>(slot->n_chunks, 128u);
+  // two 544-thread CTAs per SM; a CTA walks several chunks when there are more than that
+  static const int max_grid = [] {
+    const char* v = getenv("PPC_XOR_SEND_CTAS");
+    return v && *v ? std::max(1, atoi(v)) : 296;
+  }();
+  const int grid = (int)std::min<uint32_t>(slot->n_chunks, (uint32_t)max_grid);
   const cudaError_t e = ppc::launch_k(
-      ppc::xor_send_kernel, grid, ppc::kThreads, s, true, static_cast<uint8_t*>(slot->payload),
+      ppc::xor_send_kernel, grid, ppc::kWsThreads, s, true, static_cast<uint8_t*>(slot->payload),
       reinterpret_cast<uint64_t*>(slot->flags), (uint64_t)slot->seq,
       static_cast<const uint8_t*>(in), (uint64_t)bytes, (uint64_t)slot->chunk_bytes,
       (uint32_t)slot->n_chunks,

@@ -393,3 +393,28 @@ def test_c2_full_size_sampled(direct, monkeypatch):
         c.disconnect()
     for c in comms:
         c.destroy()
+
+
+@pytest.mark.parametrize("K", [1, 3])
+def test_batched_receive_virtual_stages(K):
+    """ppc_pp_recv_batch on event-ordered virtual stages (ring path): all n sends enqueued
+    first (WOULD_BLOCK otherwise), ragged sizes, bit-exact."""
+    sizes = [5, 3 * 65536 + 17, 65536, (1 << 20) + 3]
+    comms = _pair(max_msg_bytes=2 << 20, ring_slots=max(K, len(sizes)), chunk_bytes=64 << 10)
+    s = torch.cuda.current_stream()
+    outs = [_buf(n) for n in sizes]
+    assert comms[1].pp_recv(ppc.FWD, outs[0], sizes[0], 0, s) == ppc.WOULD_BLOCK
+    srcs = []
+    for i, n in enumerate(sizes):
+        b = _buf(n)
+        srcs.append(b)
+        ppc.fill_payload(b, n, 42, 0, 0, 0, i)
+        comms[0].send(ppc.FWD, b, n, mb=i, stream=s)
+    comms[1].recv_batch(ppc.FWD, outs, sizes, mb0=0, stream=s)
+    for i, n in enumerate(sizes):
+        assert np.array_equal(_host(outs[i])[:n], P.payload_bytes(42, 0, 0, 0, i, n)), i
+    for c in comms:
+        assert c.poll() == 0
+        c.disconnect()
+    for c in comms:
+        c.destroy()

@@ -535,3 +535,55 @@ def test_full_size_c2_zero_copy_graph():
     for g in graphs:
         g.destroy()
     _close(comms)
+
+
+@pytest.mark.parametrize("zc", [False, True])
+@pytest.mark.parametrize("K", [2, 3])
+def test_batched_receive(zc, K):
+    """ppc_pp_recv_batch: one grid receives n consecutive messages (ragged sizes, n > K so the
+    ring wraps inside one batch and the sender waits for the batch's own credits), both
+    directions at once; zc: registered sources (zc_async: the sender publishes ahead), else
+    SM push into the ring.  Every message byte-exact and recorded once, in order."""
+    sizes = [4096 + 3, 3 * (256 << 10) + 5, 1, (2 << 20) + 17, 256 << 10, 5, 777777, 64 << 10]
+    comms = _comms(max_msg_bytes=4 << 20, chunk_bytes=256 << 10, ring_slots=K,
+                   zc_async=1 if zc else 0, trace=1)
+    src = {r: [_buf(n) for n in sizes] for r in (0, 1)}
+    for r in (0, 1):
+        for i, n in enumerate(sizes):
+            ppc.fill_payload(src[r][i], n, 42, 0, 0, r, i)
+    if zc:
+        ppc.register_local(comms, [src[0], src[1]])
+    st = [torch.cuda.Stream() for _ in range(4)]
+    outs = {}
+    for d, (snd, rcv) in ((ppc.FWD, (0, 1)), (ppc.BWD, (1, 0))):
+        outs[d] = [_buf(n) for n in sizes]
+        comms[rcv].recv_batch(d, outs[d][:5], sizes[:5], mb0=0, stream=st[2 * rcv + 1])
+        comms[rcv].recv_batch(d, outs[d][5:], sizes[5:], mb0=5, stream=st[2 * rcv + 1])
+    for d, (snd, rcv) in ((ppc.FWD, (0, 1)), (ppc.BWD, (1, 0))):
+        for i, n in enumerate(sizes):
+            comms[snd].send(d, src[snd][i], n, mb=i, stream=st[2 * snd])
+        comms[snd].wait_consumed(d, st[2 * snd])
+    torch.cuda.synchronize()
+    for d in (ppc.FWD, ppc.BWD):
+        for i, n in enumerate(sizes):
+            assert np.array_equal(_host(outs[d][i])[:n], P.payload_bytes(42, 0, 0, d, i, n)), (d, i)
+    for r, c in enumerate(comms):
+        assert c.poll() == 0, c.error_info()
+        recs = [x for x in c.trace() if x["kind"] == 1]
+        assert [x["seq"] for x in recs] == list(range(1, len(sizes) + 1))
+        assert [x["mb"] for x in recs] == list(range(len(sizes)))
+    _close(comms)
+
+
+def test_batched_receive_header_error():
+    """A wrong size inside a batch latches SIZE_MISMATCH with that message's seq."""
+    comms = _comms(max_msg_bytes=1 << 20, timeout_ns=2_000_000_000)
+    s0, s1 = torch.cuda.Stream(), torch.cuda.Stream()
+    src = _buf(8192)
+    outs = [_buf(8192) for _ in range(3)]
+    for i in range(3):
+        comms[0].send(ppc.FWD, src, 8192, mb=i, stream=s0)
+    comms[1].recv_batch(ppc.FWD, outs, [8192, 8192, 4096], mb0=0, stream=s1)
+    torch.cuda.synchronize()
+    assert comms[1].error_info()[:2] == ("SIZE_MISMATCH", 3)
+    _close(comms, expect_ok=False)
