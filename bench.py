@@ -386,6 +386,7 @@ class Pipeline:
                     ppc.fill_payload(self.X[s][m], nb, 42, 0, 0xFF, 0, m)
                 if s in self.G:
                     ppc.fill_payload(self.G[s][m], nb, 42, 0, 0xFF, 1, m)
+        torch.cuda.synchronize()           # inputs (legacy stream) before the stage streams
         self.args = [ppc.StepArgs(M, nb, nb, x=self.X.get(s), g=self.G.get(s),
                                   y=self.Y.get(s), dx=self.DX.get(s)) for s in self.stages]
         self.streams = [torch.cuda.Stream() for _ in self.stages]

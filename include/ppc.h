@@ -48,6 +48,10 @@
  *   PPC_COPY_TMA_CTAS=0  virtual stages: >0 selects the TMA bulk hand-off copy with that
  *                        many CTAs (16-B aligned buffers); 0 = the SIMT copy kernel
  *                        (faster inside the overlapped step, profiles/r56_copy_engine_ab.jsonl)
+ *   PPC_WAIT_VALUE=0     eager credit waits (zero-copy rendezvous, ppc_pp_wait_consumed) as
+ *                        cuStreamWaitValue64 instead of the bounded 1-thread kernel: zero SMs,
+ *                        but UNBOUNDED (no timeout) — measured opt-in, DESIGN.md §7
+ *   PPC_XOR_SEND_CTAS=296  grid cap of the fused XOR-send kernel
  *   PPC_RECV_CTAS, PPC_STAGE_CTAS, PPC_PUSH_WS=1   grid / kernel-variant overrides
  */
 #ifndef PPC_H_

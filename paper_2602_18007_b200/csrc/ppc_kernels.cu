@@ -16,6 +16,7 @@
 #include <cstdint>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include "ppc_internal.h"
 
@@ -1043,8 +1044,35 @@ cudaError_t launch_copy(void* dst, const void* src, uint64_t bytes, uint64_t chu
                   static_cast<const uint8_t*>(src), bytes, chunk);
 }
 
+// PPC_WAIT_VALUE=1 (opt-in, eager enqueues only): the credit wait becomes a stream memory
+// operation, cuStreamWaitValue64(GEQ) — zero SMs, no kernel.  It cannot be bounded (no
+// timeout: a lost credit hangs the stream instead of latching PPC_ERR_TIMEOUT), and
+// its value is fixed at enqueue, so graph captures (device-relative sequence numbers) keep
+// the bounded 1-thread kernel.  Measured against the kernel in DESIGN.md §7.
+int g_wait_value = 0;
+namespace {
+using WaitValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+WaitValueFn wait_value_fn() {
+  static WaitValueFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (WaitValueFn) nullptr;
+    return reinterpret_cast<WaitValueFn>(f);
+  }();
+  return fn;
+}
+}  // namespace
+
 cudaError_t launch_wait_credit(const uint64_t* credit, uint64_t target, ErrWord* err,
                                uint64_t timeout_ns, cudaStream_t s, const uint64_t* seq_base) {
+  if (g_wait_value && !seq_base) {
+    if (WaitValueFn fn = wait_value_fn()) {
+      return fn((CUstream)s, (CUdeviceptr)(uintptr_t)credit, (cuuint64_t)target,
+                CU_STREAM_WAIT_VALUE_GEQ) == CUDA_SUCCESS ? cudaSuccess : cudaErrorUnknown;
+    }
+  }
   return launch_k(wait_credit_kernel, 1, 1, s, true, credit, target, err, timeout_ns, seq_base);
 }
 

@@ -198,7 +198,7 @@ def case_toy(rank, world, bf16=True, steps=5):
     M = 4
     Ws, bs = init_params(42)
     X, T = data(M, 42)
-    st = ToyStage(rank, ROWS, WIDTH, M, 10.0, bf16, rank, Ws[2 * rank:2 * rank + 2],
+    st = ToyStage(rank, ROWS, WIDTH, M, 10.0, bf16, dev(rank), Ws[2 * rank:2 * rank + 2],
                   bs[2 * rank:2 * rank + 2], X if rank == 0 else T)
     cfg = ppc.make_config(pp=2, max_msg_bytes=st.boundary_bytes, chunk_bytes=64 << 10)
     comm = ppc.connect_distributed(cfg, rank, world, dev(rank), with_nccl=False)

@@ -178,6 +178,7 @@ def _xor_step(S, M, n, K=2, chunk=64 << 10, engine=ppc.ENGINE_SM, trace=0):
     for m in range(M):
         ppc.fill_payload(X[m], n, 42, 0, P.SRC_BOUNDARY, 0, m)
         ppc.fill_payload(G[m], n, 42, 0, P.SRC_BOUNDARY, 1, m)
+    torch.cuda.synchronize()        # inputs (legacy stream) before the stage streams
     ctx = [(ppc.XorCtx(42, 0, s, 0), ppc.XorCtx(42, 0, s, 1)) for s in range(S)]
     args = [ppc.StepArgs(M, n, n, fwd=ppc.STAGE_XOR, bwd=ppc.STAGE_XOR, fwd_user=ctx[s][0],
                          bwd_user=ctx[s][1], x=X if s == 0 else None, g=G if s == S - 1 else None,
@@ -310,6 +311,7 @@ def test_step_with_host_buffers(S, fn, direct, monkeypatch):
     for _ in range(3):
         for t in hY + hDX:
             t.zero_()
+        torch.cuda.synchronize()
         ppc.step_1f1b_local(comms, args, streams)
         torch.cuda.synchronize()
         for m in range(M):
@@ -338,6 +340,7 @@ def test_xor_step_cuda_graph(S, direct, monkeypatch):
     for m in range(M):
         ppc.fill_payload(X[m], n, 42, 0, P.SRC_BOUNDARY, 0, m)
         ppc.fill_payload(G[m], n, 42, 0, P.SRC_BOUNDARY, 1, m)
+    torch.cuda.synchronize()        # inputs (legacy stream) before the stage streams
     ctx = [(ppc.XorCtx(42, 0, s, 0), ppc.XorCtx(42, 0, s, 1)) for s in range(S)]
     args = [ppc.StepArgs(M, n, n, fwd=ppc.STAGE_XOR, bwd=ppc.STAGE_XOR, fwd_user=ctx[s][0],
                          bwd_user=ctx[s][1], x=X if s == 0 else None, g=G if s == S - 1 else None,
@@ -354,6 +357,7 @@ def test_xor_step_cuda_graph(S, direct, monkeypatch):
             assert np.array_equal(_host(DX[m])[:n], ref[m][1]), m
             Y[m].fill_(0)
             DX[m].fill_(0)
+        torch.cuda.synchronize()
 
     ppc.step_1f1b_local(comms, args, streams)        # eager step: allocates step buffers
     check()

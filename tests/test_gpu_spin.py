@@ -74,6 +74,9 @@ def test_send_recv_device_spins(engine, K):
         for i, n in enumerate(sizes):
             outs[(d, i)] = _buf(n)
             outs[(d, i)].fill_(0xAB)
+    torch.cuda.synchronize()        # the fills (legacy stream) before the receives
+    for d, (snd, rcv) in ((ppc.FWD, (0, 1)), (ppc.BWD, (1, 0))):
+        for i, n in enumerate(sizes):
             comms[rcv].recv(d, outs[(d, i)], n, mb=i, stream=st[(rcv, "recv")])
     srcs = []
     for d, (snd, rcv) in ((ppc.FWD, (0, 1)), (ppc.BWD, (1, 0))):
@@ -156,6 +159,7 @@ def _xor_args(comms, S, M, n, host_io=False, fn=True):
     else:
         Y = [_buf(n) for _ in range(M)]
         DX = [_buf(n) for _ in range(M)]
+    torch.cuda.synchronize()        # inputs (legacy stream) ready before the stage streams
     ctx = [(ppc.XorCtx(42, 0, s, 0), ppc.XorCtx(42, 0, s, 1)) for s in range(S)]
     args = [ppc.StepArgs(M, n, n, fwd=ppc.STAGE_XOR if fn else None,
                          bwd=ppc.STAGE_XOR if fn else None,
@@ -205,6 +209,7 @@ def test_per_rank_step_driver_xor(engine, S, M, K):
             assert np.array_equal(Yo[m], y) and np.array_equal(DXo[m], g)
             Y[m].fill_(0)
             DX[m].fill_(0)
+        torch.cuda.synchronize()
     for c in comms:
         assert c.poll() == 0, c.error_info()
         recs = [r for r in c.trace() if r["kind"] == 1]
@@ -235,6 +240,7 @@ def test_zero_copy_publication_and_pull(mode, monkeypatch):
     for r in (0, 1):
         for i, n in enumerate(sizes):
             ppc.fill_payload(src[r][i], n, 42, 0, 0, r, i)
+    torch.cuda.synchronize()
     ppc.register_local(comms, [src[0], src[1]])
     st = [torch.cuda.Stream() for _ in range(4)]
     outs = {}
@@ -261,6 +267,7 @@ def test_zero_copy_publication_and_pull(mode, monkeypatch):
             assert np.array_equal(_host(DX[m])[:n], P.source_gradient(42, 0, m, n)), m
             Y[m].fill_(0)
             DX[m].fill_(0)
+        torch.cuda.synchronize()
     # zero-copy receive records start when the publication is seen
     for c in comms:
         assert all(r["t_end_ns"] >= r["t_start_ns"] > 0 for r in c.trace() if r["kind"] == 1)
@@ -300,6 +307,7 @@ def test_zero_copy_async_stream():
     for r in (0, 1):
         for i, n in enumerate(sizes):
             ppc.fill_payload(src[r][i], n, 42, 0, 0, r, i)
+    torch.cuda.synchronize()
     ppc.register_local(comms, [src[0], src[1]])
     st = [torch.cuda.Stream() for _ in range(4)]
     outs = {}
@@ -341,6 +349,7 @@ def test_per_rank_cuda_graph(S, zc):
             assert np.array_equal(_host(DX[m])[:n], DXo[m]), m
             Y[m].fill_(0)
             DX[m].fill_(0)
+        torch.cuda.synchronize()
 
     _step_all(comms, args, streams)              # eager step: allocates the step buffers
     check()
@@ -371,6 +380,7 @@ def test_per_rank_step_host_buffers(S, fn):
     for _ in range(3):
         for t in Y + DX:
             t.zero_()
+        torch.cuda.synchronize()
         _step_all(comms, args, streams)
         torch.cuda.synchronize()
         for m in range(M):
@@ -460,6 +470,7 @@ def test_tp_sliced_gather():
         fulls[r] = [_buf(total) for _ in range(M)]
         for m in range(M):
             ppc.fill_payload(fulls[r][m], total, 42, 0, P.SRC_BOUNDARY, d_send, m)
+    torch.cuda.synchronize()
     ppc.register_local(comms, [fulls[r] for r in range(len(comms))])
     st = {(r, k): torch.cuda.Stream() for r in range(len(comms)) for k in (0, 1)}
     for m in range(M):
@@ -532,6 +543,7 @@ def test_full_size_c2_zero_copy_graph():
             assert dig(dx) == ref_dx_d[m] and np.array_equal(dx[-4096:], ref_dx[m][-4096:]), m
             Y[m].fill_(0)
             DX[m].fill_(0)
+        torch.cuda.synchronize()
     for g in graphs:
         g.destroy()
     _close(comms)
@@ -551,6 +563,7 @@ def test_batched_receive(zc, K):
     for r in (0, 1):
         for i, n in enumerate(sizes):
             ppc.fill_payload(src[r][i], n, 42, 0, 0, r, i)
+    torch.cuda.synchronize()
     if zc:
         ppc.register_local(comms, [src[0], src[1]])
     st = [torch.cuda.Stream() for _ in range(4)]

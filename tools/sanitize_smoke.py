@@ -1,7 +1,10 @@
-"""Small one-GPU workload for compute-sanitizer (one tool per gpurun call):
-    python tools/sanitize_smoke.py && compute-sanitizer --tool memcheck python tools/sanitize_smoke.py
-Covers the ring push/recv (SM, CE, PULL engines, misaligned and ragged sizes), the direct
-single-copy step, a CUDA-graph replay and the XOR stage kernels, checked against synth."""
+"""Small one-GPU workload for compute-sanitizer (memcheck / racecheck / synccheck):
+    python tools/sanitize_smoke.py [--spin] && compute-sanitizer --tool memcheck python tools/sanitize_smoke.py
+Covers the ring push/recv (SM, CE, PULL engines, misaligned and ragged sizes), the batched
+receive, the direct single-copy step, a CUDA-graph replay and the XOR stage kernels, checked
+against synth.  --spin adds smoke()'s cross-process-protocol paths (device-spin ring and
+zero-copy with fused publication on one GPU), which need the sender's and the receiver's
+kernels to run concurrently (a tool that serialises kernels turns them into TIMEOUTs)."""
 import os
 import sys
 
@@ -16,7 +19,8 @@ from synth import payload as P  # noqa: E402
 
 
 def main():
-    __graft_entry__.smoke()
+    if "--spin" in sys.argv:
+        __graft_entry__.smoke()
     s = torch.cuda.current_stream()
     for eng in (ppc.ENGINE_SM, ppc.ENGINE_CE, ppc.ENGINE_PULL):
         comms = ppc.virtual_stages(ppc.make_config(pp=2, max_msg_bytes=1 << 20, chunk_bytes=64 << 10,
@@ -29,6 +33,18 @@ def main():
             comms[1].recv(ppc.FWD, dst.data_ptr() + off, n, mb=i, stream=s)
             torch.cuda.synchronize()
             assert np.array_equal(dst.cpu().numpy()[off:off + n], P.payload_bytes(42, 0, 0, 0, i, n))
+        sizes = [5, 3 * (64 << 10) + 7, 64 << 10]
+        outs = [torch.zeros(n, dtype=torch.uint8, device="cuda") for n in sizes]
+        srcs = []
+        for i, n in enumerate(sizes):
+            b = torch.empty(n, dtype=torch.uint8, device="cuda")
+            srcs.append(b)
+            ppc.fill_payload(b, n, 42, 0, 0, 0, 10 + i)
+            comms[0].send(ppc.FWD, b, n, mb=10 + i, stream=s)
+        comms[1].recv_batch(ppc.FWD, outs, sizes, mb0=10, stream=s)      # batched receive
+        torch.cuda.synchronize()
+        for i, n in enumerate(sizes):
+            assert np.array_equal(outs[i].cpu().numpy(), P.payload_bytes(42, 0, 0, 0, 10 + i, n))
         for c in comms:
             assert c.poll() == 0
             c.disconnect()
