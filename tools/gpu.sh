@@ -23,8 +23,8 @@ for step in "$@"; do
   case $name in
     build)    timeout 600 python paper_2602_18007_b200/build.py > "$log" 2>&1 ;;
     tests)    if [ -n "$arg" ]; then timeout 2400 python -m pytest tests -m gpu -q -k "$arg" > "$log" 2>&1
-              else timeout 2400 python -m pytest tests -m gpu -q --durations=25 > "$log" 2>              else timeout 2400 python -m pytest tests -m gpu -q > "$log" 2>&1; fi ;;1; fi ;;
-    file)     timeout 2400 python -m pytest "$arg" -m gpu -q --durations=15 > "$log" 2>    file)     timeout 2400 python -m pytest "$arg" -m gpu -q > "$log" 2>&1 ;;1 ;;
+              else timeout 2400 python -m pytest tests -m gpu -q --durations=25 > "$log" 2>&1; fi ;;
+    file)     timeout 2400 python -m pytest "$arg" -m gpu -q --durations=15 > "$log" 2>&1 ;;
     smoke)    timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$log" 2>&1 ;;
     bench1)   timeout 600 python bench.py > "$log" 2>&1 ;;
     benchN)   PORT=$((PORT+1)); timeout 600 python -m torch.distributed.run --nnodes=1 \
