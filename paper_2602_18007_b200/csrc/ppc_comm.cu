@@ -687,10 +687,13 @@ ppc_status_t ppc_pp_recv(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t bytes, lo
   return ppc_impl_recv_ex(c, d, buf, bytes, mb, s, nullptr);
 }
 
-// pub != nullptr: the receive kernel also publishes that (prepared) zero-copy send once
-// this receive has completed (step driver fusion, ppc_step.cu)
-ppc_status_t ppc_impl_recv_ex(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t bytes,
-                              long long mb, cudaStream_t s, const PublishArgs* pub) {
+// Arguments of the next receive of direction d (bookkeeping included: recv_seq advances,
+// trace record taken).  pub != nullptr: the receive kernel also publishes that (prepared)
+// zero-copy send once this receive has completed (step driver fusion, ppc_step.cu).
+// Virtual stages: the stream waits for the matching send's event first.
+ppc_status_t ppc_impl_recv_prepare(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t bytes,
+                                   long long mb, cudaStream_t s, const PublishArgs* pub,
+                                   RecvArgs* out) {
   ppc_status_t st = check_live(c);
   if (st) return st;
   if (d != PPC_FWD && d != PPC_BWD) return PPC_ERR_INVALID_ARG;
@@ -699,7 +702,7 @@ ppc_status_t ppc_impl_recv_ex(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t byte
   if (h.peer_in < 0) return PPC_ERR_NO_NEIGHBOR;
   if (bytes > c->cfg.max_msg_bytes) return PPC_ERR_TOO_LARGE;
   if (c->device < 0) return PPC_ERR_STATE;
-  DeviceGuard g(c->device);
+  if (pub && c->local_mode) return PPC_ERR_STATE;
   const uint64_t seq = h.recv_seq + 1;
   const int slot = (int)(seq % c->K);
   if (c->local_mode) {
@@ -709,7 +712,8 @@ ppc_status_t ppc_impl_recv_ex(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t byte
       CK(cudaStreamWaitEvent(s, sh.sent_ev[slot], 0));
   }
   const uint32_t n_chunks = (uint32_t)((bytes + c->chunk - 1) / c->chunk);
-  RecvArgs a{};
+  RecvArgs& a = *out;
+  a = RecvArgs{};
   a.dst = static_cast<uint8_t*>(buf);
   a.src = h.i_payload + (size_t)slot * c->lay.stride;
   a.hdr = h.i_hdr + slot;
@@ -731,7 +735,6 @@ ppc_status_t ppc_impl_recv_ex(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t byte
       ? c->seg_tab + ((size_t)(d == PPC_FWD ? 0 : 1) * c->cfg.tp + c->tp_i) * kMaxSeg : nullptr;
   a.peer_arena = h.i_arena;
   if (pub) {
-    if (c->local_mode) return PPC_ERR_STATE;
     a.has_pub = 1;
     a.pub = *pub;
   }
@@ -745,11 +748,44 @@ ppc_status_t ppc_impl_recv_ex(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t byte
     a.flags = h.i_flags;
     a.done = h.i_done;
   }
-  if (ppc_status_t ts = time_mark(c, 1, s, true)) return ts;
-  CK(launch_recv(a, recv_grid(c, n_chunks), c->sys_scope, s));
-  if (ppc_status_t ts = time_mark(c, 1, s, false)) return ts;
   h.recv_seq = seq;
-  if (c->local_mode) CK(cudaEventRecord(h.recvd_ev[slot], s));
+  return PPC_OK;
+}
+
+// After the receive kernel of direction d (seq = the channel's current recv_seq) is enqueued.
+ppc_status_t ppc_impl_recv_done(ppc_comm_t* c, ppc_dir_t d, uint64_t seq, cudaStream_t s) {
+  if (c->local_mode) CK(cudaEventRecord(c->ch[d].recvd_ev[seq % c->K], s));
+  return PPC_OK;
+}
+
+ppc_status_t ppc_impl_recv_ex(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t bytes,
+                              long long mb, cudaStream_t s, const PublishArgs* pub) {
+  if (!c) return PPC_ERR_STATE;
+  DeviceGuard g(c->device);
+  RecvArgs a;
+  ppc_status_t st = ppc_impl_recv_prepare(c, d, buf, bytes, mb, s, pub, &a);
+  if (st) return st;
+  if (ppc_status_t ts = time_mark(c, 1, s, true)) return ts;
+  CK(launch_recv(a, recv_grid(c, a.n_chunks), c->sys_scope, s));
+  if (ppc_status_t ts = time_mark(c, 1, s, false)) return ts;
+  return ppc_impl_recv_done(c, d, c->ch[d].recv_seq, s);
+}
+
+// A batch of prepared receives (each possibly with a fused publication) in ONE grid.
+ppc_status_t ppc_impl_recv_launch_batch(ppc_comm_t* c, const RecvArgs* as, int n,
+                                        cudaStream_t s) {
+  if (n < 1 || n > kMaxBatch) return PPC_ERR_INVALID_ARG;
+  DeviceGuard g(c->device);
+  static thread_local RecvBatch b;       // ~6 KiB: kept off the stack
+  b.n = (uint32_t)n;
+  uint32_t max_chunks = 1;
+  for (int i = 0; i < n; ++i) {
+    b.a[i] = as[i];
+    max_chunks = std::max(max_chunks, as[i].n_chunks);
+  }
+  if (ppc_status_t ts = time_mark(c, 1, s, true)) return ts;
+  CK(launch_recv_batch(b, recv_grid(c, max_chunks), c->sys_scope, s));
+  if (ppc_status_t ts = time_mark(c, 1, s, false)) return ts;
   return PPC_OK;
 }
 
@@ -762,69 +798,19 @@ ppc_status_t ppc_pp_recv_batch(ppc_comm_t* c, ppc_dir_t d, void* const* bufs,
   Chan& h = c->ch[d];
   if (h.peer_in < 0) return PPC_ERR_NO_NEIGHBOR;
   if (c->device < 0) return PPC_ERR_STATE;
-  uint32_t max_chunks = 1;
-  for (int i = 0; i < n; ++i) {
+  for (int i = 0; i < n; ++i) {        // every argument error before anything is enqueued
     if (bytes[i] > 0 && !bufs[i]) return PPC_ERR_INVALID_ARG;
     if (bytes[i] > c->cfg.max_msg_bytes) return PPC_ERR_TOO_LARGE;
-    max_chunks = std::max<uint32_t>(max_chunks, (uint32_t)((bytes[i] + c->chunk - 1) / c->chunk));
   }
+  if (c->local_mode && h.in_comm->ch[d].send_seq < h.recv_seq + n) return PPC_ERR_WOULD_BLOCK;
   DeviceGuard g(c->device);
-  if (c->local_mode) {                   // virtual stages: every message's send enqueued
-    Chan& sh = h.in_comm->ch[d];
-    if (sh.send_seq < h.recv_seq + n) return PPC_ERR_WOULD_BLOCK;
-    for (int i = 0; i < n; ++i) {
-      const uint64_t seq = h.recv_seq + 1 + i;
-      if (!(c->capturing && seq <= h.in_comm->cap_send[d]))
-        CK(cudaStreamWaitEvent(s, sh.sent_ev[seq % c->K], 0));
-    }
-  }
-  static thread_local RecvBatch b;       // ~8 KiB: kept off the stack
-  memset(&b, 0, sizeof(b));
-  b.n = (uint32_t)n;
-  for (int i = 0; i < n; ++i) {
-    const uint64_t seq = h.recv_seq + 1 + i;
-    const int slot = (int)(seq % c->K);
-    RecvArgs& a = b.a[i];
-    a.dst = static_cast<uint8_t*>(bufs[i]);
-    a.src = h.i_payload + (size_t)slot * c->lay.stride;
-    a.hdr = h.i_hdr + slot;
-    a.hdr_flag = h.i_hdr_flag + slot;
-    a.flags = h.i_flags + (size_t)slot * std::max<uint32_t>(c->lay.max_chunks, 1);
-    a.peer_credit = h.peer_credit;
-    a.done = h.i_done + slot;
-    a.bytes = bytes[i];
-    a.chunk = c->chunk;
-    a.n_chunks = (uint32_t)((bytes[i] + c->chunk - 1) / c->chunk);
-    a.seq = seq;
-    a.mb = mb0 + i;
-    a.err = c->err_dev;
-    a.timeout_ns = c->timeout_ns;
-    a.rec = next_record(c);
-    a.rec_src = h.peer_in;
-    a.rec_dst = c->rank;
-    a.seg_tab = c->seg_tab
-        ? c->seg_tab + ((size_t)(d == PPC_FWD ? 0 : 1) * c->cfg.tp + c->tp_i) * kMaxSeg : nullptr;
-    a.peer_arena = h.i_arena;
-    if (c->capturing) {                  // graph: relative seq, slot resolved on device
-      a.sr = {c->dseq + 2 + d, (uint64_t)c->lay.stride, (uint32_t)c->K,
-              std::max<uint32_t>(c->lay.max_chunks, 1), 0, 0};
-      a.seq = seq - c->cap_recv[d];
-      a.src = h.i_payload;
-      a.hdr = h.i_hdr;
-      a.hdr_flag = h.i_hdr_flag;
-      a.flags = h.i_flags;
-      a.done = h.i_done;
-    }
-  }
-  if (ppc_status_t ts = time_mark(c, 1, s, true)) return ts;
-  CK(launch_recv_batch(b, recv_grid(c, max_chunks), c->sys_scope, s));
-  if (ppc_status_t ts = time_mark(c, 1, s, false)) return ts;
-  h.recv_seq += (uint64_t)n;
-  if (c->local_mode)
-    for (int i = 0; i < n; ++i) {
-      const uint64_t seq = h.recv_seq - n + 1 + i;
-      CK(cudaEventRecord(h.recvd_ev[seq % c->K], s));
-    }
+  RecvArgs as[kMaxBatch];
+  for (int i = 0; i < n; ++i)
+    if ((st = ppc_impl_recv_prepare(c, d, bufs[i], bytes[i], mb0 + i, s, nullptr, &as[i])))
+      return st;
+  if ((st = ppc_impl_recv_launch_batch(c, as, n, s))) return st;
+  for (int i = 0; i < n; ++i)
+    if ((st = ppc_impl_recv_done(c, d, h.recv_seq - n + 1 + i, s))) return st;
   return PPC_OK;
 }
 

@@ -211,6 +211,14 @@ ppc_status_t ppc_impl_zc_commit(ppc_comm_t* c, const ZcSend& z, cudaStream_t s,
 // ppc_pp_recv whose kernel also publishes `pub` after completing (nullptr: plain receive)
 ppc_status_t ppc_impl_recv_ex(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t bytes,
                               long long mb, cudaStream_t s, const PublishArgs* pub);
+// the same split in three: arguments + bookkeeping, one grid for n prepared receives, and
+// the per-message completion bookkeeping (virtual stages: the recvd event)
+ppc_status_t ppc_impl_recv_prepare(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t bytes,
+                                   long long mb, cudaStream_t s, const PublishArgs* pub,
+                                   RecvArgs* out);
+ppc_status_t ppc_impl_recv_launch_batch(ppc_comm_t* c, const RecvArgs* as, int n,
+                                        cudaStream_t s);
+ppc_status_t ppc_impl_recv_done(ppc_comm_t* c, ppc_dir_t d, uint64_t seq, cudaStream_t s);
 }
 
 namespace ppc_impl {

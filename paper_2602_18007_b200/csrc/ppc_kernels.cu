@@ -632,7 +632,11 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(const __grid_constant__ 
   const uint8_t* zc_src = s_zc_src;
   // the early pull is valid only for the message resolved now (CTA-uniform condition)
   const bool use_pre = kEarly && pre_ok && zc_src == s_early_src && s_early_seq == a.seq;
-  for (uint32_t c = blockIdx.x; c < a.n_chunks; c += gridDim.x) {
+  // fused publication: block 0 spends the start on the next op's header (credit wait, NVLink
+  // stores, system fence); it carries no chunks, else it would be the tail CTA whose
+  // completion gates the publication (launch_recv adds one CTA for it)
+  const uint32_t w0 = (kPub && !kEarly) ? 1u : 0u;
+  for (uint32_t c = blockIdx.x - w0; blockIdx.x >= w0 && c < a.n_chunks; c += gridDim.x - w0) {
     const uint64_t off = (uint64_t)c * a.chunk;
     const uint64_t len = min(a.chunk, a.bytes - off);
     if (zc_src) {                      // payload complete at publication: pull it over NVLink
@@ -681,10 +685,16 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(const __grid_constant__ 
 // order without extra waiting: the last CTA of message i+1 counted itself after finishing
 // message i, which it did after its own arrival on i (fence + atomic chain), so credit i is
 // stored before credit i+1.
-template <bool kSys>
+// kPub (the step driver's batched terminal receives): message i may carry a fused
+// publication of the stage's next zero-copy send, exactly as recv_kernel<kSys, true>: block 0
+// writes its header when it reaches message i (and carries no chunks), the message's last
+// CTA releases its header flag together with the receive's credit.
+template <bool kSys, bool kPub>
 __global__ void __launch_bounds__(kThreads) recv_batch_kernel(const __grid_constant__ RecvBatch b) {
   __shared__ const uint8_t* s_zc_src;
   pdl_enter();
+  const uint32_t w0 = kPub ? 1u : 0u;            // block 0: publication headers only
+  const uint32_t workers = gridDim.x - w0;
   for (uint32_t i = 0; i < b.n; ++i) {
     const RecvArgs a = resolve(b.a[i]);
     int fail = 0;
@@ -695,7 +705,9 @@ __global__ void __launch_bounds__(kThreads) recv_batch_kernel(const __grid_const
       s_zc_src = nullptr;
       if (a.rec && blockIdx.x == 0)
         fill_record(a.rec, (long long)t0, a.rec_src, a.rec_dst, -1, 1, a.seq, a.mb, a.bytes);
-      if (!wait_geq<kSys>(a.hdr_flag, a.seq, deadline)) {
+      if (kPub && blockIdx.x == 0 && a.has_pub && !fused_publish_header(&b.a[i].pub)) {
+        fail = 1;
+      } else if (!wait_geq<kSys>(a.hdr_flag, a.seq, deadline)) {
         latch(a.err, PPC_ERR_TIMEOUT, a.seq, 0x100u);
         fail = 1;
       } else {
@@ -722,21 +734,24 @@ __global__ void __launch_bounds__(kThreads) recv_batch_kernel(const __grid_const
     const uint8_t* zc_src = s_zc_src;
     // rotate the chunk ownership per message so the CTAs that carried the last chunks of
     // one message start the next one early
-    const uint32_t first = (blockIdx.x + i * (a.n_chunks % gridDim.x)) % gridDim.x;
-    for (uint32_t c = first; c < a.n_chunks; c += gridDim.x) {
-      const uint64_t off = (uint64_t)c * a.chunk;
-      const uint64_t len = min(a.chunk, a.bytes - off);
-      if (zc_src) {
-        cta_copy<true>(a.dst + off, zc_src + off, len);
-        continue;
+    if (blockIdx.x >= w0) {
+      const uint32_t wid = blockIdx.x - w0;
+      const uint32_t first = (wid + i * (a.n_chunks % workers)) % workers;
+      for (uint32_t c = first; c < a.n_chunks; c += workers) {
+        const uint64_t off = (uint64_t)c * a.chunk;
+        const uint64_t len = min(a.chunk, a.bytes - off);
+        if (zc_src) {
+          cta_copy<true>(a.dst + off, zc_src + off, len);
+          continue;
+        }
+        int f = 0;
+        if (threadIdx.x == 0 && !wait_geq<kSys>(a.flags + c, a.seq, deadline)) {
+          latch(a.err, PPC_ERR_TIMEOUT, a.seq, 0x100u | c << 12);
+          f = 1;
+        }
+        if (__syncthreads_or(f)) return;
+        cta_copy<true>(a.dst + off, a.src + off, len);
       }
-      int f = 0;
-      if (threadIdx.x == 0 && !wait_geq<kSys>(a.flags + c, a.seq, deadline)) {
-        latch(a.err, PPC_ERR_TIMEOUT, a.seq, 0x100u | c << 12);
-        f = 1;
-      }
-      if (__syncthreads_or(f)) return;
-      cta_copy<true>(a.dst + off, a.src + off, len);
     }
     __threadfence();
     __syncthreads();
@@ -744,7 +759,11 @@ __global__ void __launch_bounds__(kThreads) recv_batch_kernel(const __grid_const
       if (atomicAdd(a.done, 1u) == gridDim.x - 1) {
         *a.done = 0;
         __threadfence();
-        st_rel<kSys>(a.peer_credit, a.seq);
+        if (kPub && a.has_pub) {
+          fused_publish_flag(&b.a[i].pub, a.peer_credit, a.seq);
+        } else {
+          st_rel<kSys>(a.peer_credit, a.seq);
+        }
         if (a.rec) a.rec->t_end_ns = (long long)globaltimer();
       }
     }
@@ -752,9 +771,12 @@ __global__ void __launch_bounds__(kThreads) recv_batch_kernel(const __grid_const
 }
 
 cudaError_t launch_recv_batch(const RecvBatch& b, int grid, bool sys, cudaStream_t s) {
-  auto k = sys ? recv_batch_kernel<true> : recv_batch_kernel<false>;
+  bool pub = false;
+  for (uint32_t i = 0; i < b.n; ++i) pub = pub || b.a[i].has_pub;
+  auto k = pub ? (sys ? recv_batch_kernel<true, true> : recv_batch_kernel<false, true>)
+               : (sys ? recv_batch_kernel<true, false> : recv_batch_kernel<false, false>);
   if (sys) grid = std::min(grid, kMaxSpinGrid);
-  grid = fit_grid(k, grid, kThreads);
+  grid = fit_grid(k, grid + (pub ? 1 : 0), kThreads);
   return launch_k(k, grid, kThreads, s, pdl_fits(k, grid, kThreads), b);
 }
 
@@ -1091,11 +1113,12 @@ cudaError_t launch_recv(const RecvArgs& a, int grid, bool sys, cudaStream_t s) {
                      : (sys ? recv_kernel<true, false> : recv_kernel<false, false>);
   if (sys) grid = std::min(grid, kMaxSpinGrid);
   grid = fit_grid(k, grid, kThreads);
-  const bool pdl = pdl_fits(k, grid, kThreads);
   if (sys && g_pdl && g_recv_early) {   // zero-copy pulls over NVLink; without PDL nothing runs early
     auto ke = a.has_pub ? recv_kernel<true, true, true> : recv_kernel<true, false, true>;
     if (pdl_fits(ke, grid, kThreads)) return launch_k(ke, grid, kThreads, s, true, a);
   }
+  if (a.has_pub) grid = fit_grid(k, grid + 1, kThreads);   // + the header-only block 0
+  const bool pdl = pdl_fits(k, grid, kThreads);
   return launch_k(k, grid, kThreads, s, pdl, a);
 }
 cudaError_t launch_ce_head(const CeHeadArgs& a, cudaStream_t s, bool pdl) {
@@ -1124,7 +1147,8 @@ cudaError_t preload_kernels() {
       (const void*)recv_kernel<true, false>, (const void*)recv_kernel<false, false>,
       (const void*)recv_kernel<true, false, true>, (const void*)recv_kernel<true, true, true>,
       (const void*)recv_kernel<true, true>,  (const void*)recv_kernel<false, true>,
-      (const void*)recv_batch_kernel<true>, (const void*)recv_batch_kernel<false>,
+      (const void*)recv_batch_kernel<true, false>, (const void*)recv_batch_kernel<false, false>,
+      (const void*)recv_batch_kernel<true, true>, (const void*)recv_batch_kernel<false, true>,
       (const void*)gather_kernel,          (const void*)publish_kernel,
       (const void*)ce_head_kernel,         (const void*)ce_flags_kernel,
       (const void*)wait_credit_kernel,     (const void*)set_seq_kernel,

@@ -117,6 +117,44 @@ struct Stepper {
   bool used_ds = false;         // a terminal output went to host memory through sb.ds
   bool dmode = false;
   cudaStream_t xq = nullptr;    // direct mode: the GPU's transfer queue (nullptr: own stream)
+  // PPC_STEP_BATCH=1 (one process per GPU): consecutive terminal receives (identity stage,
+  // device destination — with the next op's zero-copy publication fused in or not) whose
+  // ops enqueue nothing else on the compute stream are collected and launched as ONE
+  // batched-receive grid (ppc_impl_recv_launch_batch), so the receiving CTAs flow from one
+  // message to the next without a kernel boundary.  Their rendezvous commits and completion
+  // bookkeeping follow the grid.
+  bool batching = false;
+  std::vector<RecvArgs> pend;
+  std::vector<std::pair<int, uint64_t>> pend_done;   // (dir, seq)
+  std::vector<ZcSend> pend_commit;
+
+  ppc_status_t flush() {
+    if (pend.empty()) return PPC_OK;
+    for (size_t b = 0; b < pend.size(); b += kMaxBatch) {
+      const int n = (int)std::min<size_t>(kMaxBatch, pend.size() - b);
+      if (ppc_status_t st = ppc_impl_recv_launch_batch(c, pend.data() + b, n, cs)) return st;
+    }
+    for (auto& dq : pend_done)
+      if (ppc_status_t st = ppc_impl_recv_done(c, (ppc_dir_t)dq.first, dq.second, cs)) return st;
+    for (const ZcSend& z : pend_commit) {
+      if (ppc_status_t ts = time_mark(c, 0, cs, true)) return ts;
+      if (ppc_status_t ws = ppc_impl_zc_commit(c, z, cs, c->side[z.d])) return ws;
+      if (ppc_status_t ts = time_mark(c, 0, c->side[z.d], false)) return ts;
+    }
+    pend.clear();
+    pend_done.clear();
+    pend_commit.clear();
+    return PPC_OK;
+  }
+
+  // the op's input is a terminal identity receive into a device destination
+  bool terminal_recv(int kind, int m) const {
+    const bool has_in = kind == 0 ? s > 0 : s < S - 1;
+    const bool has_out = kind == 0 ? s < S - 1 : s > 0;
+    void* const* dsts = kind == 0 ? st->y : st->dx;
+    return has_in && !has_out && !(kind == 0 ? st->fwd : st->bwd) && dsts && dsts[m] &&
+           !is_host_ptr(dsts[m]);
+  }
 
   ppc_status_t init(ppc_comm* comm, const ppc_step_t* step, cudaStream_t stream) {
     c = comm;
@@ -218,6 +256,30 @@ struct Stepper {
       const bool has_in = kind == 0 ? s > 0 : s < S - 1;
       const bool has_out = kind == 0 ? s < S - 1 : s > 0;
       const int bi = m & 1;
+      // batched terminal receives: anything else that enqueues on the compute stream first
+      // launches the pending batch (a fused source op enqueues nothing there)
+      const bool batchable = batching && phase == 0 && terminal_recv(kind, m);
+      if (batching && phase == 0 && !batchable && !fused_next)
+        if (ppc_status_t fs = flush()) return fs;
+      if (batchable) {
+        void* dst = (kind == 0 ? st->y : st->dx)[m];
+        ZcSend z;
+        const bool fuse = fusable_next(&z);
+        RecvArgs ra;
+        if (ppc_status_t rs = ppc_impl_recv_prepare(c, (ppc_dir_t)d, dst, bytes, m, cs,
+                                                    fuse ? &z.p : nullptr, &ra))
+          return rs;
+        pend.push_back(ra);
+        pend_done.push_back({d, c->ch[d].recv_seq});
+        if (fuse) {
+          pend_commit.push_back(z);
+          fused_next = true;
+        }
+        direct = true;
+        in = dst;
+        *progressed = true;
+        phase = 1;
+      }
       if (phase == 0) {                                  // input
         direct = false;
         if (has_in) {
@@ -438,6 +500,7 @@ struct Stepper {
   }
 
   ppc_status_t finish() {
+    if (ppc_status_t fs = flush()) return fs;
     if (used_ds) {                 // host outputs complete with the step
       CK(cudaEventRecord(c->sb.djoin, c->sb.ds));
       CK(cudaStreamWaitEvent(cs, c->sb.djoin, 0));
@@ -468,6 +531,7 @@ extern "C" ppc_status_t ppc_step_1f1b(ppc_comm_t* c, const ppc_step_t* st, cudaS
   DeviceGuard g(c->device);
   Stepper sp;
   if ((r = sp.init(c, st, s))) return r;
+  sp.batching = env_int("PPC_STEP_BATCH", 0) != 0;
   while (!sp.done()) {
     bool prog = false;
     if ((r = sp.advance(&prog))) return r;

@@ -107,3 +107,10 @@ def test_full_size_bench_configuration(n):
 def test_tp_sliced_boundary_fused_gather():
     """NEXT-1 on 4 GPUs (PP=2 x TP=2)."""
     _run("gather", 4)
+
+
+@pytest.mark.parametrize("case", ["zc", "graph"])
+def test_step_batched_terminal_receives(case):
+    """PPC_STEP_BATCH=1: each rank's terminal receives (and their fused publications) run as
+    one batched-receive grid per step, eager and inside the step's CUDA graph."""
+    _run(case, 2, env={"PPC_STEP_BATCH": "1"})

@@ -220,7 +220,7 @@ def test_per_rank_step_driver_xor(engine, S, M, K):
     _close(comms)
 
 
-@pytest.mark.parametrize("mode", ["fused", "unfused", "side", "early"])
+@pytest.mark.parametrize("mode", ["fused", "unfused", "side", "early", "batch"])
 def test_zero_copy_publication_and_pull(mode, monkeypatch):
     """Registered send buffers: the sender only publishes (segment, offset) in the receiver's
     slot header, the receiver pulls the payload straight into its buffer.  Ragged messages
@@ -229,9 +229,10 @@ def test_zero_copy_publication_and_pull(mode, monkeypatch):
     publishes from the preceding terminal receive kernel (default); unfused: its own
     publication kernel (PPC_FUSE_PUBLISH=0); side: publication on the send stream
     (PPC_ZC_SIDE=1); early: receives look for the publication before griddepcontrol.wait
-    (PPC_RECV_EARLY=1)."""
+    (PPC_RECV_EARLY=1); batch: the step's terminal receives with their fused publications
+    as one batched-receive grid (PPC_STEP_BATCH=1)."""
     env = {"unfused": ("PPC_FUSE_PUBLISH", "0"), "side": ("PPC_ZC_SIDE", "1"),
-           "early": ("PPC_RECV_EARLY", "1")}
+           "early": ("PPC_RECV_EARLY", "1"), "batch": ("PPC_STEP_BATCH", "1")}
     if mode in env:
         monkeypatch.setenv(*env[mode])
     comms = _comms(max_msg_bytes=8 << 20, chunk_bytes=256 << 10, trace=1)
@@ -325,13 +326,16 @@ def test_zero_copy_async_stream():
     _close(comms)
 
 
+@pytest.mark.parametrize("batch", [0, 1])
 @pytest.mark.parametrize("S", [2, 3])
 @pytest.mark.parametrize("zc", [False, True])
-def test_per_rank_cuda_graph(S, zc):
+def test_per_rank_cuda_graph(S, zc, batch, monkeypatch):
     """Each rank's step captured into its own CUDA graph (ppc_graph_create with n = 1, the
     one-process-per-GPU form; device-side sequence bases), replayed interleaved with eager
     steps.  zc: identity stages with registered X / G (zero-copy pulls and the fused
-    publication inside the graphs); otherwise XOR stages over the ring."""
+    publication inside the graphs); otherwise XOR stages over the ring.  batch: terminal
+    receives as one batched-receive grid per step (PPC_STEP_BATCH=1)."""
+    monkeypatch.setenv("PPC_STEP_BATCH", str(batch))
     M, n = 4, 3 * (256 << 10) + 99
     comms = _comms(pp=S, max_msg_bytes=n, chunk_bytes=256 << 10)
     args, X, G, Y, DX = _xor_args(comms, S, M, n, fn=not zc)
@@ -512,12 +516,14 @@ def test_hetero_allreduce_leader_chain(S):
     _close(comms)
 
 
-def test_full_size_c2_zero_copy_graph():
+@pytest.mark.parametrize("batch", [0, 1])
+def test_full_size_c2_zero_copy_graph(batch, monkeypatch):
     """BASELINE configs[1] at full size in bench.py's N >= 2 launch configuration, run on one
     GPU: [1,4096,4096] bf16 (32 MiB) messages, PP = 2, M = 8, registered X / G (zero-copy
     pulls, 256 KiB grain, fused publication), each rank's step replayed as a CUDA graph.
     ALL 8 Y and 8 DX compared with the oracle byte for byte (blake2b of the full buffers
-    plus first / last 4 KiB), over three replays."""
+    plus first / last 4 KiB), over three replays.  batch: PPC_STEP_BATCH=1."""
+    monkeypatch.setenv("PPC_STEP_BATCH", str(batch))
     S, M, n = 2, 8, 4096 * 4096 * 2
     comms = _comms(pp=S, max_msg_bytes=n, chunk_bytes=256 << 10)
     args, X, G, Y, DX = _xor_args(comms, S, M, n, fn=False)
