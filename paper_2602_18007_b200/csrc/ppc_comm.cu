@@ -198,6 +198,10 @@ ppc_status_t ppc_create(const ppc_config_t* cfg, int world, int rank, int cuda_d
     if (preload_kernels() != cudaSuccess) return fail(PPC_ERR_CUDA);   // no lazy loads later
     if (cudaMalloc(&c->arena, c->lay.total) != cudaSuccess) return fail(PPC_ERR_CUDA);
     if (cudaMemset(c->arena, 0, c->lay.total) != cudaSuccess) return fail(PPC_ERR_CUDA);
+    // the same for the driver's device-to-device copy (CE engine, host staging): its first
+    // use must not be a lazy load that waits for a device on which a receive is spinning
+    if (cudaMemcpy(c->arena + c->lay.step, c->arena, 64, cudaMemcpyDeviceToDevice) != cudaSuccess)
+      return fail(PPC_ERR_CUDA);
     if (cudaHostAlloc(&c->err_host, sizeof(ErrHost), cudaHostAllocMapped) != cudaSuccess)
       return fail(PPC_ERR_CUDA);
     memset(c->err_host, 0, sizeof(ErrHost));

@@ -1139,6 +1139,7 @@ __global__ void __launch_bounds__(kWsThreads) xor_send_kernel(uint8_t* out, uint
                                                               uint64_t seq, const uint8_t* in,
                                                               uint64_t bytes, uint64_t chunk,
                                                               uint32_t n_chunks, uint64_t key);
+__global__ void splitmix_xor_kernel(uint8_t* out, const uint8_t* in, uint64_t bytes, uint64_t key);
 cudaError_t preload_kernels() {
   cudaFuncAttributes fa;
   const void* fns[] = {
@@ -1155,6 +1156,7 @@ cudaError_t preload_kernels() {
       (const void*)add_kernel<float>,      (const void*)add_kernel<__half>,
       (const void*)add_kernel<__nv_bfloat16>, (const void*)add_kernel<int32_t>,
       (const void*)copy_kernel,            (const void*)xor_send_kernel,
+      (const void*)splitmix_xor_kernel,
   };
   for (const void* f : fns) {
     const cudaError_t e = cudaFuncGetAttributes(&fa, f);

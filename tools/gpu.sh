@@ -12,7 +12,10 @@
 #   ref            bench.py --impl reference
 #   launches       ncu launch list (gpu__time_duration) of the N = 1 bench
 #   ncu:REGEX      ncu --set full of the first launch of kernel REGEX in the N = 1 bench
-#   py:SCRIPT ARGS python SCRIPT (args after the colon, comma separated)
+#   py:SCRIPT,ARGS python SCRIPT (args after the colon, comma separated)
+#   trun:N,SCRIPT,ARGS   torchrun N ranks of SCRIPT (comma separated)
+#   env:K=V        export K=V for the following steps
+#   sh:CMD         any shell command (commas become spaces)
 TAG=$1; shift
 mkdir -p gpurun_out
 PORT=29700
@@ -38,6 +41,11 @@ for step in "$@"; do
                 -s 4 -c 1 -o gpurun_out/${TAG}_prof_$(echo "$arg" | tr -c 'A-Za-z0-9\n' '_') \
                 python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > "$log" 2>&1 ;;
     py)       timeout 1200 python ${arg//,/ } > "$log" 2>&1 ;;
+    trun)     PORT=$((PORT+1)); n=${arg%%,*}; rest=${arg#*,}
+              timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node "$n" \
+                --master-addr 127.0.0.1 --master-port $PORT ${rest//,/ } > "$log" 2>&1 ;;
+    env)      export "$arg"; echo "export $arg" > "$log" ;;
+    sh)       timeout 1200 bash -c "${arg//,/ }" > "$log" 2>&1 ;;
     *)        echo "unknown step $step" > "$log" ;;
   esac
   echo "rc=$?" >> "$log"
