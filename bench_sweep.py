@@ -195,7 +195,7 @@ def main():
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
     fh = open(a.out.replace(".jsonl", f".r{rank}.jsonl"), "w")
     maxn = max(sizes)
-    for spec in [x for x in a.sm.split(",") if x]:
+    for spec in [x for x in a.sm.split(",") if x and x != "none"]:
         cta, chunk = spec.split(":")
         cfg = ppc.make_config(pp=world, max_msg_bytes=maxn, chunk_bytes=size_of(chunk),
                               cta_per_channel=int(cta), engine=ppc.ENGINE_SM)
@@ -206,7 +206,7 @@ def main():
         comm.disconnect()
         dist.barrier()
         comm.destroy()
-    for ch in [x for x in a.ce.split(",") if x]:
+    for ch in [x for x in a.ce.split(",") if x and x != "none"]:
         cfg = ppc.make_config(pp=world, max_msg_bytes=maxn, chunk_bytes=MiB, channels=int(ch),
                               engine=ppc.ENGINE_CE)
         comm = ppc.connect_distributed(cfg, rank, world, torch.cuda.current_device(),

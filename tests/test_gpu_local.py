@@ -191,13 +191,11 @@ def _xor_step(S, M, n, K=2, chunk=64 << 10, engine=ppc.ENGINE_SM, trace=0):
 
 
 @pytest.mark.parametrize("S,M", [(2, 1), (2, 4), (3, 4), (4, 8), (5, 3)])
-@pytest.mark.parametrize("engine", [ppc.ENGINE_SM, ppc.ENGINE_CE, ppc.ENGINE_PULL])
-@pytest.mark.parametrize("direct", [0, 1])
+@pytest.mark.parametrize("engine,direct", [(ppc.ENGINE_SM, 0), (ppc.ENGINE_CE, 0),
+                                           (ppc.ENGINE_PULL, 0), (ppc.ENGINE_SM, 1)])
 def test_xor_1f1b_step_matches_oracle(S, M, engine, direct, monkeypatch):
-    """direct=0: the ring path (push -> flags -> copy-out); direct=1: the single-copy hand-off
-    of same-GPU virtual stages."""
-    if direct and engine != ppc.ENGINE_SM:
-        pytest.skip("direct mode does not use the engine")
+    """direct=0: the ring path (push -> flags -> copy-out) of each engine; direct=1: the
+    single-copy hand-off of same-GPU virtual stages (no engine involved)."""
     monkeypatch.setenv("PPC_LOCAL_DIRECT", str(direct))
     n = 3 * (64 << 10) + 1234                          # several chunks + ragged tail
     comms, Y, DX = _xor_step(S, M, n, engine=engine, trace=1)
