@@ -135,7 +135,8 @@ typedef struct { int kind; /* 0 = F, 1 = B */ int mb; } ppc_op_t;
 
 typedef struct {
   long long t_start_ns, t_end_ns;   /* %globaltimer of the first CTA start / last CTA end     */
-  int src, dst, dir, kind;          /* kind: 0 = send, 1 = recv                                */
+  int src, dst, dir, kind;          /* kind: 0 = send, 1 = recv; a recv's dir is -1, or -2 when
+                                       PPC_RECV_EARLY's early look found the publication      */
   long long seq, mb, bytes;
 } ppc_record_t;
 

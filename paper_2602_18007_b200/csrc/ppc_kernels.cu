@@ -587,8 +587,8 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(const __grid_constant__ 
   if (kEarly && threadIdx.x == 0 && s_early_src && s_early_seq == a.seq) {
     // header already checked in the early phase (same seq, so the same slot and message)
     s_zc_src = s_early_src;
-    if (a.rec && blockIdx.x == 0) {
-      fill_record(a.rec, (long long)globaltimer(), a.rec_src, a.rec_dst, -1, 1, a.seq, a.mb, a.bytes);
+    if (a.rec && blockIdx.x == 0) {  // dir -2 in the record: the early look hit (ppc_trace)
+      fill_record(a.rec, (long long)globaltimer(), a.rec_src, a.rec_dst, -2, 1, a.seq, a.mb, a.bytes);
       a.rec->t_start_ns = (long long)globaltimer();
     }
     if (kPub && blockIdx.x == 0 && !fused_publish_header(&a0.pub)) fail = 1;

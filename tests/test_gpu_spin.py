@@ -606,3 +606,33 @@ def test_batched_receive_header_error():
     torch.cuda.synchronize()
     assert comms[1].error_info()[:2] == ("SIZE_MISMATCH", 3)
     _close(comms, expect_ok=False)
+
+
+def test_early_receive_hits_and_stays_exact(monkeypatch):
+    """PPC_RECV_EARLY=1: three zero-copy messages from distinct registered buffers
+    are published BEFORE their receives are enqueued back to back on one stream, so the
+    receives after the first find their publication in the early look (record dir = -2) and
+    pull their first 64 KiB per CTA before griddepcontrol.wait; bytes exact either way."""
+    monkeypatch.setenv("PPC_RECV_EARLY", "1")
+    n = 4 << 20
+    comms = _comms(max_msg_bytes=n, chunk_bytes=256 << 10, zc_async=1, trace=1)
+    srcs = [_buf(n) for _ in range(3)]
+    for i, b in enumerate(srcs):
+        ppc.fill_payload(b, n, 42, 0, 0, 0, i)
+    torch.cuda.synchronize()
+    ppc.register_local(comms, [srcs, []])
+    s0, s1 = torch.cuda.Stream(), torch.cuda.Stream()
+    for i in range(3):
+        comms[0].send(ppc.FWD, srcs[i], n, mb=i, stream=s0)
+    torch.cuda.synchronize()                    # all three published
+    outs = [_buf(n) for _ in range(3)]
+    for i in range(3):
+        comms[1].recv(ppc.FWD, outs[i], n, mb=i, stream=s1)
+    comms[0].wait_consumed(ppc.FWD, s0)
+    torch.cuda.synchronize()
+    for i in range(3):
+        assert np.array_equal(_host(outs[i]), P.payload_bytes(42, 0, 0, 0, i, n)), i
+    recs = [r for r in comms[1].trace() if r["kind"] == 1]
+    assert [r["seq"] for r in recs] == [1, 2, 3]
+    assert sum(r["dir"] == -2 for r in recs) >= 1, recs
+    _close(comms)
