@@ -53,6 +53,10 @@ def main():
     ap.add_argument("--pp", type=int, default=0, help="0 = world / tp")
     ap.add_argument("--tp", type=int, default=1)
     ap.add_argument("--layers", type=int, default=1, help="MLP blocks per stage")
+    ap.add_argument("--layers-per-stage", default="",
+                    help="comma list, one count per stage (overrides --layers): uneven splits")
+    ap.add_argument("--ffn-scale-stage0", type=float, default=1.0,
+                    help="stage 0's ffn width x this (a slower stage, the paper's AMD side)")
     ap.add_argument("--hidden", type=int, default=4096)
     ap.add_argument("--ffn", type=int, default=14336)
     ap.add_argument("--M", type=int, default=8)
@@ -60,6 +64,8 @@ def main():
     ap.add_argument("--reps", type=int, default=3, help="alternating full / control repeats")
     ap.add_argument("--engine", default="sm")
     ap.add_argument("--layer-times", action="store_true")
+    ap.add_argument("--comm-gbps", type=float, default=643.0,
+                    help="planner: per-message transfer rate (measured N=2 pull data phase)")
     ap.add_argument("--out", default="gpurun_out/exposure.jsonl")
     ap.add_argument("--inplace", action="store_true",
                     help="PPC_STEP_INPLACE=1: stage fns produce straight into the peer's slot")
@@ -75,11 +81,17 @@ def main():
     assert world % (S * TP) == 0
     M, T, H, F = a.M, 4096, a.hidden, a.ffn // TP
     nbytes = T * H * 2
+    per_stage = [int(x) for x in a.layers_per_stage.split(",")] if a.layers_per_stage else [a.layers] * S
+    assert len(per_stage) == S
+    stage_of = lambda r: r // (TP * (world // (S * TP)))      # rank = pp_i * tp * dp + ...
+    L = per_stage[stage_of(rank)]
+    if stage_of(rank) == 0:
+        F = int(round(F * a.ffn_scale_stage0 / 64)) * 64
     g = torch.Generator(device="cuda").manual_seed(42 + rank)
     W1 = [torch.randn(H, F, device="cuda", dtype=torch.bfloat16, generator=g) * 0.02
-          for _ in range(a.layers)]
+          for _ in range(L)]
     W2 = [torch.randn(F, H, device="cuda", dtype=torch.bfloat16, generator=g) * 0.02
-          for _ in range(a.layers)]
+          for _ in range(L)]
     x0 = torch.randn(T, H, device="cuda", dtype=torch.bfloat16, generator=g)
     eng = {"sm": ppc.ENGINE_SM, "pull": ppc.ENGINE_PULL, "ce": ppc.ENGINE_CE}[a.engine]
     cfg = ppc.make_config(tp=TP, pp=S, dp=world // (S * TP), max_msg_bytes=nbytes,
@@ -101,8 +113,8 @@ def main():
         with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
             h = x0 if inp is None else inp.view(T, H)
             for r in range(reps):
-                for l in range(a.layers):
-                    last = out is not None and r == reps - 1 and l == a.layers - 1
+                for l in range(L):
+                    last = out is not None and r == reps - 1 and l == L - 1
                     # the last GEMM's epilogue stores straight into `out` (with
                     # PPC_STEP_INPLACE: the receiver's ring slot, over NVLink)
                     h = block(h, l, out.view(T, H) if last else None)
@@ -161,7 +173,7 @@ def main():
     dist.all_gather_object(layers_all, layer)
     if rank == 0:
         pp_bytes = 2 * M * nbytes if 0 < stage < S - 1 else M * nbytes   # sent per step
-        rec = {"pp": S, "tp": TP, "dp": world // (S * TP), "M": M, "layers_per_stage": a.layers,
+        rec = {"pp": S, "tp": TP, "dp": world // (S * TP), "M": M, "layers_per_stage": per_stage,
                "engine": a.engine, "produce_in_place": a.inplace,
                "ms_step": full, "ms_step_flags_only": ctrl,
                "exposed_frac": (full - ctrl) / full,
@@ -179,6 +191,24 @@ def main():
                           "no attention / norms"}
         if a.layer_times:
             rec["layer_ms"] = layers_all
+            # NEXT-3: the planner fed with these measured per-layer
+            # times — its predicted step time for this split vs the measured one, and the
+            # split it recommends for the same total layer count
+            from paper_2602_18007_b200.partition import iteration_time, optimize_partition
+            by_stage = {}
+            for r, lt in enumerate(layers_all):
+                by_stage.setdefault(stage_of(r), lt)
+            tf = [by_stage[st]["fwd"] for st in range(S)]
+            tb = [by_stage[st]["bwd"] for st in range(S)]
+            comm_ms = nbytes / (a.comm_gbps * 1e9) * 1e3        # one boundary message
+            rec["planner"] = {
+                "layers_per_stage": per_stage, "t_fwd_ms": tf, "t_bwd_ms": tb,
+                "predicted_ms_step": iteration_time(per_stage, tf, tb, M, comm_ms),
+                "measured_ms_step": full,
+                "recommended_split": optimize_partition(sum(per_stage), tf, tb, M, comm_ms),
+                "ffn_scale_stage0": a.ffn_scale_stage0,
+                "model": "paper_2602_18007_b200.partition.iteration_time (1F1B event model, "
+                         "per-layer fwd/bwd ms measured alone on each stage)"}
         print(json.dumps(rec), flush=True)
         os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
         with open(a.out, "a") as fh:
