@@ -742,12 +742,16 @@ def main():
                      "timed_region": "per-launch data phase (%globaltimer, publication seen -> "
                                      "last CTA); event_* = CUDA events around the launch, "
                                      "which include the wait for the peer's publication",
-                     "traffic": ncu_traffic("recv_n2")})
+                     "traffic": ncu_traffic("recv_n2"),
+                     "traffic_counters": "ncu nvlrx__bytes_data_user.sum + nvltx__bytes_data_user"
+                                         ".sum per launch (profiles/ncu_traffic.json)"})
     elif roof is not None:
         roof.update({"kernel": "ppc::push_ws_kernel (SM push over NVLink)",
                      "achieved": roof["event_achieved"], "avg_launch_us": roof["event_launch_us"],
                      "timed_region": "CUDA events around every push launch (instrumented pass)",
-                     "traffic": ncu_traffic("push_n2")})
+                     "traffic": ncu_traffic("push_n2"),
+                     "traffic_counters": "ncu nvltx__bytes_data_user.sum + nvlrx__bytes_data_user"
+                                         ".sum per launch (profiles/ncu_traffic.json)"})
     if roof is not None:
         roof["frac"] = roof["achieved"] / roof["peak"]
 
