@@ -780,9 +780,12 @@ def main():
     if not args.no_extra:
         for name in EXTRA.get(ctx.world, []):
             wx = resolve(args, ctx.world, name)
-            px, r = measure(ctx, wx, max(3, args.steps // 2), max(3, args.warmup))
-            r["outputs_checked"] = px.outputs_ok()
-            px.close()
+            try:                        # a side measurement must not sink the headline line
+                px, r = measure(ctx, wx, max(3, args.steps // 2), max(3, args.warmup))
+                r["outputs_checked"] = px.outputs_ok()
+                px.close()
+            except Exception as e:
+                r = {"error": repr(e)[:300]}
             r["config"] = config_dict(wx, ctx.world)
             extra[name] = r
 

@@ -134,6 +134,16 @@ def main():
     if a.layer_times:
         ts = {"fwd": [], "bwd": []}
         with torch.cuda.stream(s):
+            # sustained clocks: ~1 s of back-to-back blocks first (a power-capped B200 runs
+            # long GEMM streams below its burst clock, and the pipeline step is such a stream)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            h = block(x0, 0, None)
+            e1.record(s)
+            torch.cuda.synchronize()
+            for _ in range(max(1, int(1000.0 / max(e0.elapsed_time(e1), 0.05)))):
+                h = block(x0, 0, None)
+            torch.cuda.synchronize()
             for kind, reps in (("fwd", 1), ("bwd", 2)):
                 for i in range(12):
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

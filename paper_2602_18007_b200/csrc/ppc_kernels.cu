@@ -814,10 +814,14 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(GatherArgs a) {
     }
   }
   if (__syncthreads_or(fail)) return;
-  // every CTA pulls (slice, chunk) units of all TP senders over NVLink into its slot of dst
+  // every CTA pulls (slice, chunk) units of all TP senders over NVLink into its slot of dst.
+  // Units interleave the senders (consecutive units come from different senders) and each
+  // receiver starts at its own TP index, so at any time a receiver pulls from every sender
+  // and every sender serves every receiver — not all receivers draining sender 0 first
+  // (measured: 322 GB/s per receiver sender-major vs the replicated boundary's 607)
   const uint32_t units = a.tp * a.n_chunks;
   for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
-    const uint32_t t = u / a.n_chunks, c = u % a.n_chunks;
+    const uint32_t t = (u + a.my_tp) % a.tp, c = u / a.tp;
     const uint64_t off = (uint64_t)c * a.chunk;
     const uint64_t len = min(a.chunk, a.slice_bytes - off);
     cta_copy<true>(a.dst + (uint64_t)t * a.slice_bytes + off, s_src[t] + off, len);
