@@ -560,6 +560,7 @@ ppc_status_t ppc_impl_send_ex(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_
     a.rec_src = c->rank;
     a.rec_dst = h.peer_out;
     a.done = h.push_done;
+    a.channels = (uint32_t)std::max(1, c->cfg.channels);
     if (c->capturing) {           // graph: relative seq, slot resolved on device
       a.sr = {c->dseq + d, (uint64_t)c->lay.stride, (uint32_t)c->K,
               std::max<uint32_t>(c->lay.max_chunks, 1), c->local_mode ? 0u : 1u, 0};
@@ -738,6 +739,7 @@ ppc_status_t ppc_impl_recv_prepare(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t
   a.seg_tab = c->seg_tab
       ? c->seg_tab + ((size_t)(d == PPC_FWD ? 0 : 1) * c->cfg.tp + c->tp_i) * kMaxSeg : nullptr;
   a.peer_arena = h.i_arena;
+  a.channels = c->cfg.engine == PPC_ENGINE_CE ? 1u : (uint32_t)std::max(1, c->cfg.channels);
   if (pub) {
     a.has_pub = 1;
     a.pub = *pub;

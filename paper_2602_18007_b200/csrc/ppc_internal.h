@@ -78,6 +78,7 @@ struct PushArgs {
   ppc_record_t* rec;            // trace record or nullptr
   int rec_src, rec_dst;
   uint32_t* done;               // completion counter (trace only)
+  uint32_t channels;            // MPDT channels: contiguous chunk ranges per CTA group
 };
 
 // Zero-copy publication of a registered send buffer: credit wait, header, header flag.
@@ -115,6 +116,7 @@ struct RecvArgs {
   int rec_src, rec_dst;
   const uint64_t* seg_tab;      // zero-copy: mapped bases of the sender's registered buffers
   const uint8_t* peer_arena;    // zero-copy from the sender's arena (src_seg == kArenaSeg)
+  uint32_t channels;            // MPDT channels of the pulling / copy-out CTAs
   // fused publication (step driver): when has_pub, the last CTA publishes `pub` (the next
   // op's zero-copy send) right after releasing this receive's credit
   uint32_t has_pub;

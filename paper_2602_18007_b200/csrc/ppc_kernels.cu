@@ -267,6 +267,24 @@ __device__ __forceinline__ void cta_copy(uint8_t* __restrict__ dst, const uint8_
   }
 }
 
+// ---------------------------------------------------------------- MPDT channels
+// The paper splits one message across several NICs (Multi-NIC Parallel Data Transfer).  Here
+// a message's chunks are split into C contiguous ranges ("channels"), each moved by its own
+// group of CTAs: CTA b of `workers` serves channel b % C and walks chunks [c0, c1) of that
+// channel with a stride of the channel's CTA count.  C = 1 is the plain grid stride.
+struct ChanIter {
+  uint32_t first, end, step;
+};
+__device__ __forceinline__ ChanIter chan_iter(uint32_t n_chunks, uint32_t C, uint32_t b,
+                                              uint32_t workers) {
+  C = max(1u, min(C, workers));
+  const uint32_t ch = b % C;
+  const uint32_t ctas = (workers - ch + C - 1) / C;          // CTAs serving channel ch
+  const uint32_t c0 = (uint32_t)((uint64_t)n_chunks * ch / C);
+  const uint32_t c1 = (uint32_t)((uint64_t)n_chunks * (ch + 1) / C);
+  return {c0 + b / C, c1, ctas};
+}
+
 // ---------------------------------------------------------------- graph-replay resolution
 // (SeqRef): absolute seq and slot pointers from the device sequence base.
 __device__ __forceinline__ PushArgs resolve(PushArgs a) {
@@ -336,7 +354,8 @@ __global__ void __launch_bounds__(kThreads) push_kernel(PushArgs a0) {
     }
   }
   if (__syncthreads_or(fail)) return;
-  for (uint32_t c = blockIdx.x; c < a.n_chunks; c += gridDim.x) {
+  const ChanIter it = chan_iter(a.n_chunks, a.channels, blockIdx.x, gridDim.x);
+  for (uint32_t c = it.first; c < it.end; c += it.step) {
     const uint64_t off = (uint64_t)c * a.chunk;
     const uint64_t len = min(a.chunk, a.bytes - off);
     cta_copy<false>(a.dst + off, a.src + off, len);
@@ -426,10 +445,11 @@ __global__ void __launch_bounds__(kWsThreads) push_ws_kernel(PushArgs a0) {
   }
   if (__syncthreads_or(fail)) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const ChanIter it = chan_iter(a.n_chunks, a.channels, blockIdx.x, gridDim.x);
   uint32_t i = 0;
   if (warp == 0) {                                   // signal warp
     if (lane == 0) {
-      for (uint32_t c = blockIdx.x; c < a.n_chunks; c += gridDim.x, ++i) {
+      for (uint32_t c = it.first; c < it.end; c += it.step, ++i) {
         const int b = i % kWsRing;
         mbar_wait(&full[b], (i / kWsRing) & 1);
         fence_rel<kSys>();
@@ -439,7 +459,7 @@ __global__ void __launch_bounds__(kWsThreads) push_ws_kernel(PushArgs a0) {
     }
   } else {                                           // copy warps
     const uint64_t tid = threadIdx.x - 32, nt = 32 * kWsCopyWarps;
-    for (uint32_t c = blockIdx.x; c < a.n_chunks; c += gridDim.x, ++i) {
+    for (uint32_t c = it.first; c < it.end; c += it.step, ++i) {
       const int b = i % kWsRing;
       if (i >= kWsRing) mbar_wait(&empty[b], ((i / kWsRing) - 1) & 1);
       const uint64_t off = (uint64_t)c * a.chunk;
@@ -570,8 +590,9 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(const __grid_constant__ 
       }
     }
     __syncthreads();
-    const uint64_t off = (uint64_t)blockIdx.x * a0.chunk;
-    if (s_early_src && blockIdx.x < a0.n_chunks &&
+    const uint32_t c_first = chan_iter(a0.n_chunks, a0.channels, blockIdx.x, gridDim.x).first;
+    const uint64_t off = (uint64_t)c_first * a0.chunk;
+    if (s_early_src && c_first < chan_iter(a0.n_chunks, a0.channels, blockIdx.x, gridDim.x).end &&
         min(a0.chunk, a0.bytes - off) >= (uint64_t)kEarlyV * kThreads * sizeof(V32) &&
         (((uintptr_t)(a0.dst + off) | (uintptr_t)(s_early_src + off)) & 31) == 0) {
       const V32* src = reinterpret_cast<const V32*>(s_early_src + off);
@@ -636,12 +657,14 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(const __grid_constant__ 
   // stores, system fence); it carries no chunks, else it would be the tail CTA whose
   // completion gates the publication (launch_recv adds one CTA for it)
   const uint32_t w0 = (kPub && !kEarly) ? 1u : 0u;
-  for (uint32_t c = blockIdx.x - w0; blockIdx.x >= w0 && c < a.n_chunks; c += gridDim.x - w0) {
+  const ChanIter it = blockIdx.x >= w0 ? chan_iter(a.n_chunks, a.channels, blockIdx.x - w0,
+                                                   gridDim.x - w0) : ChanIter{0, 0, 1};
+  for (uint32_t c = it.first; c < it.end; c += it.step) {
     const uint64_t off = (uint64_t)c * a.chunk;
     const uint64_t len = min(a.chunk, a.bytes - off);
     if (zc_src) {                      // payload complete at publication: pull it over NVLink
       uint64_t skip = 0;
-      if (use_pre && c == blockIdx.x) {
+      if (use_pre && c == it.first) {
         V32* d = reinterpret_cast<V32*>(a.dst + off);
 #pragma unroll
         for (int j = 0; j < kEarlyV; ++j) st_data(d + threadIdx.x + j * kThreads, pre[j]);

@@ -636,3 +636,33 @@ def test_early_receive_hits_and_stays_exact(monkeypatch):
     assert [r["seq"] for r in recs] == [1, 2, 3]
     assert sum(r["dir"] == -2 for r in recs) >= 1, recs
     _close(comms)
+
+
+@pytest.mark.parametrize("C", [2, 3, 8])
+@pytest.mark.parametrize("mode", ["sm", "pull", "zc"])
+def test_mpdt_channels(C, mode):
+    """MPDT analogue: a message's chunks split into C contiguous channel ranges, each
+    moved by its own CTA group (push, PULL staging + pulls, zero-copy pulls); ragged sizes
+    with fewer chunks than channels, both directions, byte-exact."""
+    engine = {"sm": ppc.ENGINE_SM, "pull": ppc.ENGINE_PULL, "zc": ppc.ENGINE_SM}[mode]
+    sizes = [1, 3 * 65536 + 17, (2 << 20) + 5, 65536 * 7]
+    comms = _comms(max_msg_bytes=4 << 20, chunk_bytes=64 << 10, engine=engine, channels=C,
+                   cta_per_channel=2)
+    src = {r: [_buf(n) for n in sizes] for r in (0, 1)}
+    for r in (0, 1):
+        for i, n in enumerate(sizes):
+            ppc.fill_payload(src[r][i], n, 42, 0, 0, r, i)
+    torch.cuda.synchronize()
+    if mode == "zc":
+        ppc.register_local(comms, [src[0], src[1]])
+    st = [torch.cuda.Stream() for _ in range(4)]
+    outs = {}
+    for d, (snd, rcv) in ((ppc.FWD, (0, 1)), (ppc.BWD, (1, 0))):
+        for i, n in enumerate(sizes):
+            outs[(d, i)] = _buf(n)
+            comms[snd].send(d, src[snd][i], n, mb=i, stream=st[2 * snd])
+            comms[rcv].recv(d, outs[(d, i)], n, mb=i, stream=st[2 * rcv + 1])
+    torch.cuda.synchronize()
+    for (d, i), t in outs.items():
+        assert np.array_equal(_host(t)[:sizes[i]], P.payload_bytes(42, 0, 0, d, i, sizes[i])), (d, i)
+    _close(comms)
