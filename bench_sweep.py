@@ -39,6 +39,9 @@ def parse():
                                              "64:256K:ab (a = cfg.zc_async, sends complete at "
                                              "publication; b = batched receives, 16 per grid)")
     ap.add_argument("--modes", default="uni,bidir")
+    ap.add_argument("--channels", default="1",
+                    help="MPDT channel counts C (comma list) applied to every SM / zero-copy spec: "
+                         "the message's chunks split into C contiguous ranges, one CTA group each")
     ap.add_argument("--comparators", default="nccl,ce_copy,gloo")
     ap.add_argument("--reps", type=int, default=5)
     return ap.parse_args()
@@ -195,13 +198,15 @@ def main():
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
     fh = open(a.out.replace(".jsonl", f".r{rank}.jsonl"), "w")
     maxn = max(sizes)
-    for spec in [x for x in a.sm.split(",") if x and x != "none"]:
+    chans = [int(x) for x in a.channels.split(",")]
+    for spec, C in [(x, c) for x in a.sm.split(",") if x and x != "none" for c in chans]:
         cta, chunk = spec.split(":")
         cfg = ppc.make_config(pp=world, max_msg_bytes=maxn, chunk_bytes=size_of(chunk),
-                              cta_per_channel=int(cta), engine=ppc.ENGINE_SM)
+                              cta_per_channel=max(1, int(cta) // C), channels=C,
+                              engine=ppc.ENGINE_SM)
         comm = ppc.connect_distributed(cfg, rank, world, torch.cuda.current_device(),
                                        with_nccl=False)
-        bench_ppc(comm, rank, sizes, modes, f"ppc_sm_cta{cta}_chunk{chunk}", a.reps, fh)
+        bench_ppc(comm, rank, sizes, modes, f"ppc_sm_cta{cta}_chunk{chunk}_C{C}", a.reps, fh)
         dist.barrier()
         comm.disconnect()
         dist.barrier()
@@ -216,18 +221,18 @@ def main():
         comm.disconnect()
         dist.barrier()
         comm.destroy()
-    for spec in [x for x in a.zc.split(",") if x]:
+    for spec, C in [(x, c) for x in a.zc.split(",") if x for c in chans]:
         parts = spec.split(":")            # recv_ctas:chunk[:flags]  (a = zc_async, b = batch)
         rc, chunk = parts[0], parts[1]
         zc_async = len(parts) > 2 and "a" in parts[2]
         batch = 16 if len(parts) > 2 and "b" in parts[2] else 0
         os.environ["PPC_RECV_CTAS"] = rc
         cfg = ppc.make_config(pp=world, max_msg_bytes=maxn, chunk_bytes=size_of(chunk),
-                              zc_async=int(zc_async))
+                              zc_async=int(zc_async), channels=C)
         comm = ppc.connect_distributed(cfg, rank, world, torch.cuda.current_device(),
                                        with_nccl=False)
         label = (f"ppc_zerocopy{'_async' if zc_async else ''}{'_batch' if batch else ''}"
-                 f"_recv{rc}_chunk{chunk}")
+                 f"_recv{rc}_chunk{chunk}_C{C}")
         bench_ppc(comm, rank, sizes, modes, label, a.reps, fh, zc=True, batch=batch)
         os.environ.pop("PPC_RECV_CTAS")
         dist.barrier()
