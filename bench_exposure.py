@@ -132,29 +132,27 @@ def main():
     s = torch.cuda.Stream()
     layer = None
     if a.layer_times:
+        # sustained per-layer time: the mean over ~1 s of back-to-back blocks (a power-capped
+        # B200 runs a long GEMM stream — the pipeline step — below its burst clock, and a
+        # short timed burst after idle over-states the rate); bwd = 2 blocks (the proxy's bwd)
         ts = {"fwd": [], "bwd": []}
         with torch.cuda.stream(s):
-            # sustained clocks: ~1 s of back-to-back blocks first (a power-capped B200 runs
-            # long GEMM streams below its burst clock, and the pipeline step is such a stream)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(s)
-            h = block(x0, 0, None)
+            block(x0, 0, None)
             e1.record(s)
             torch.cuda.synchronize()
-            for _ in range(max(1, int(1000.0 / max(e0.elapsed_time(e1), 0.05)))):
-                h = block(x0, 0, None)
-            torch.cuda.synchronize()
-            for kind, reps in (("fwd", 1), ("bwd", 2)):
-                for i in range(12):
-                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    e0.record(s)
-                    h = x0
-                    for _ in range(reps):
-                        h = block(h, 0, None)
-                    e1.record(s)
-                    torch.cuda.synchronize()
-                    if i >= 2:
-                        ts[kind].append(e0.elapsed_time(e1))
+            n_blk = torch.tensor([max(10, int(1000.0 / max(e0.elapsed_time(e1), 0.05)))])
+            dist.all_reduce(n_blk, op=dist.ReduceOp.MAX)     # TP ranks call NCCL in lockstep
+            n_blk = int(n_blk.item())
+            for _ in range(3):
+                e0.record(s)
+                for _ in range(n_blk):
+                    block(x0, 0, None)
+                e1.record(s)
+                torch.cuda.synchronize()
+                ts["fwd"].append(e0.elapsed_time(e1) / n_blk)
+                ts["bwd"].append(2 * e0.elapsed_time(e1) / n_blk)
         layer = {k: statistics.median(v) for k, v in ts.items()}
 
     res = {"full": [], "flags_only": []}

@@ -440,6 +440,11 @@ void fill_publish(ppc_comm* c, ppc_dir_t d, uint64_t seq, uint64_t need, size_t 
   p.src_seg = (uint32_t)zc_seg;
   p.dir = d;
   p.boundary = (uint32_t)(d == PPC_FWD ? c->pp_i : c->pp_i - 1);
+  static const int gpu_fence = [] {
+    const char* v = getenv("PPC_PUB_FENCE");
+    return v && strcmp(v, "gpu") == 0 ? 1 : 0;
+  }();
+  p.gpu_fence = (uint32_t)gpu_fence;
   p.err = c->err_dev;
   p.timeout_ns = c->timeout_ns;
   z->d = d;

@@ -91,6 +91,8 @@ struct PublishArgs {
   uint64_t bytes, seq, src_off;
   int64_t mb;
   uint32_t src_seg, dir, boundary;
+  uint32_t gpu_fence;             // PPC_PUB_FENCE=gpu (opt-in): fused flag release without the
+                                  // system fence (the header was already fenced by block 0)
   ErrWord* err;
   uint64_t timeout_ns;
   ppc_record_t* rec;              // trace: publish kernel entry .. header flag stored

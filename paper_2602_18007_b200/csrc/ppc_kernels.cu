@@ -539,7 +539,13 @@ __device__ __forceinline__ void fused_publish_flag(const PublishArgs* p0, uint64
     flag += pseq % p0->sr.K;
   }
   const uint64_t t0 = globaltimer();
-  fence_acq_rel_sys();
+  // PPC_PUB_FENCE=gpu: block 0's header stores were already fenced at system scope before
+  // its arrival on the done counter (fused_publish_header), every CTA's pulled loads have
+  // returned before its arrival, and this CTA saw all arrivals — so only gpu-scope ordering
+  // is left to establish here.  Opt-in A/B; the default keeps the full
+  // system-scope release.
+  if (p0->gpu_fence) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  else fence_acq_rel_sys();
   st_relaxed_sys(flag, pseq);
   st_relaxed_sys(credit, seq);
   if (ppc_record_t* r = p0->rec) {
