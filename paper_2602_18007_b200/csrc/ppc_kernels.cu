@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <atomic>
+#include <cstddef>
 #include <cstdint>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -519,6 +520,31 @@ __device__ __forceinline__ void publish_body(const PublishArgs& a) {
 }
 
 // ---------------------------------------------------------------- K10: recv + copy-out
+// The 64-B slot header read in ONE round trip (two 32-B L2 loads issued together) after the
+// header flag's acquire, instead of a chain of dependent volatile field loads.
+struct HdrView {
+  uint32_t magic, flags, src_seg;
+  uint64_t bytes, seq, src_off;
+  int64_t mb;
+};
+__device__ __forceinline__ HdrView read_header(const SlotHeader* hp) {
+  const V32* v = reinterpret_cast<const V32*>(hp);
+  const V32 a = ld_ring(v), b = ld_ring(v + 1);
+  HdrView h;
+  h.magic = a.lo.x;                                    // u32 magic | u8 dir | u8 bnd | u16 flags
+  h.flags = a.lo.y >> 16;
+  h.bytes = (uint64_t)a.lo.z | (uint64_t)a.lo.w << 32;
+  h.seq = (uint64_t)a.hi.x | (uint64_t)a.hi.y << 32;
+  h.mb = (int64_t)((uint64_t)a.hi.z | (uint64_t)a.hi.w << 32);
+  h.src_off = (uint64_t)b.lo.z | (uint64_t)b.lo.w << 32;   // b: step | src_off | src_seg | pad
+  h.src_seg = b.hi.x;
+  return h;
+}
+static_assert(offsetof(SlotHeader, flags) == 6 && offsetof(SlotHeader, bytes) == 8 &&
+              offsetof(SlotHeader, seq) == 16 && offsetof(SlotHeader, mb) == 24 &&
+              offsetof(SlotHeader, src_off) == 40 && offsetof(SlotHeader, src_seg) == 48,
+              "read_header decodes the SlotHeader layout");
+
 // Fused publication.  Its arguments are read from the grid-constant parameter space right
 // where they are used, so none of them stays live in registers across the copy loop
 // (a local copy of them had pushed the kernel to 110 registers, one CTA per SM).
@@ -634,21 +660,21 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(const __grid_constant__ 
       latch(a.err, PPC_ERR_TIMEOUT, a.seq, 0x100u);
       fail = 1;
     } else {
-      const volatile SlotHeader* h = a.hdr;
-      if (h->magic != kMagic || h->seq != a.seq || h->mb != a.mb) {
+      const HdrView h = read_header(a.hdr);
+      if (h.magic != kMagic || h.seq != a.seq || h.mb != a.mb) {
         latch(a.err, PPC_ERR_ORDER, a.seq, 0x100u);
         fail = 1;
-      } else if (h->bytes != a.bytes) {
+      } else if (h.bytes != a.bytes) {
         latch(a.err, PPC_ERR_SIZE_MISMATCH, a.seq, 0x100u);
         fail = 1;
-      } else if (h->flags & kHdrZeroCopy) {
-        const uint32_t seg = h->src_seg;
+      } else if (h.flags & kHdrZeroCopy) {
+        const uint32_t seg = h.src_seg;
         const uint64_t base = zc_base(a, seg);
         if (!base) {                   // the receiver never imported that registration
           latch(a.err, PPC_ERR_ORDER, a.seq, 0x300u | seg << 12);
           fail = 1;
         } else {
-          s_zc_src = reinterpret_cast<const uint8_t*>(base + h->src_off);
+          s_zc_src = reinterpret_cast<const uint8_t*>(base + h.src_off);
           // trace: a zero-copy receive starts moving data when the publication is seen
           if (a.rec && blockIdx.x == 0) a.rec->t_start_ns = (long long)globaltimer();
         }
@@ -740,20 +766,20 @@ __global__ void __launch_bounds__(kThreads) recv_batch_kernel(const __grid_const
         latch(a.err, PPC_ERR_TIMEOUT, a.seq, 0x100u);
         fail = 1;
       } else {
-        const volatile SlotHeader* h = a.hdr;
-        if (h->magic != kMagic || h->seq != a.seq || h->mb != a.mb) {
+        const HdrView h = read_header(a.hdr);
+        if (h.magic != kMagic || h.seq != a.seq || h.mb != a.mb) {
           latch(a.err, PPC_ERR_ORDER, a.seq, 0x100u);
           fail = 1;
-        } else if (h->bytes != a.bytes) {
+        } else if (h.bytes != a.bytes) {
           latch(a.err, PPC_ERR_SIZE_MISMATCH, a.seq, 0x100u);
           fail = 1;
-        } else if (h->flags & kHdrZeroCopy) {
-          const uint64_t base = zc_base(a, h->src_seg);
+        } else if (h.flags & kHdrZeroCopy) {
+          const uint64_t base = zc_base(a, h.src_seg);
           if (!base) {
-            latch(a.err, PPC_ERR_ORDER, a.seq, 0x300u | h->src_seg << 12);
+            latch(a.err, PPC_ERR_ORDER, a.seq, 0x300u | h.src_seg << 12);
             fail = 1;
           } else {
-            s_zc_src = reinterpret_cast<const uint8_t*>(base + h->src_off);
+            s_zc_src = reinterpret_cast<const uint8_t*>(base + h.src_off);
             if (a.rec && blockIdx.x == 0) a.rec->t_start_ns = (long long)globaltimer();
           }
         }
