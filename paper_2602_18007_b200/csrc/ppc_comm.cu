@@ -215,21 +215,10 @@ ppc_status_t ppc_create(const ppc_config_t* cfg, int world, int rank, int cuda_d
     if (cudaIpcGetMemHandle(&b.ipc, c->arena) != cudaSuccess) return fail(PPC_ERR_CUDA);
     if (cudaDeviceGetPCIBusId(b.busid, sizeof(b.busid), cuda_device) != cudaSuccess)
       return fail(PPC_ERR_CUDA);
-    int lo = 0, hi = 0;
-    cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    for (int d = 0; d < 2; ++d)
-      if (cudaStreamCreateWithPriority(&c->side[d], cudaStreamNonBlocking, hi) != cudaSuccess ||
-          cudaStreamCreateWithPriority(&c->zcw[d], cudaStreamNonBlocking, hi) != cudaSuccess)
-        return fail(PPC_ERR_CUDA);
-    if (cfg->engine == PPC_ENGINE_CE) {
-      for (int i = 0; i < c->cfg.channels; ++i) {
-        if (cudaStreamCreateWithPriority(&c->ce[i], cudaStreamNonBlocking, hi) != cudaSuccess ||
-            cudaEventCreateWithFlags(&c->ce_join[i], cudaEventDisableTiming) != cudaSuccess)
-          return fail(PPC_ERR_CUDA);
-      }
-      if (cudaEventCreateWithFlags(&c->ce_fork, cudaEventDisableTiming) != cudaSuccess)
-        return fail(PPC_ERR_CUDA);
-    }
+    // send streams (side, CE channels) are created in ppc_connect for the directions that
+    // have a neighbour, the zero-copy wait streams on first use: a process that drives many
+    // comms (virtual stages) must stay under CUDA_DEVICE_MAX_CONNECTIONS hardware queues, or
+    // aliased streams add false dependencies behind spinning kernels
     if (cfg->trace && cudaMalloc(&c->trace_dev, sizeof(ppc_record_t) * kTraceCap) != cudaSuccess)
       return fail(PPC_ERR_CUDA);
     if (cudaDeviceSynchronize() != cudaSuccess) return fail(PPC_ERR_CUDA);
@@ -381,6 +370,20 @@ ppc_status_t ppc_connect(ppc_comm_t* c, const void* all_blobs, size_t blob_bytes
           CK(cudaEventCreateWithFlags(&h.sent_ev[k], cudaEventDisableTiming));
           CK(cudaEventCreateWithFlags(&h.recvd_ev[k], cudaEventDisableTiming));
         }
+      }
+    }
+    {
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      for (int d = 0; d < 2; ++d) {
+        if (c->ch[d].peer_out < 0) continue;
+        if (!c->side[d]) CK(cudaStreamCreateWithPriority(&c->side[d], cudaStreamNonBlocking, hi));
+        if (c->cfg.engine != PPC_ENGINE_CE) continue;
+        for (int i = 0; i < c->cfg.channels; ++i) {
+          if (!c->ce[d][i]) CK(cudaStreamCreateWithPriority(&c->ce[d][i], cudaStreamNonBlocking, hi));
+          if (!c->ce_join[d][i]) CK(cudaEventCreateWithFlags(&c->ce_join[d][i], cudaEventDisableTiming));
+        }
+        if (!c->ce_fork[d]) CK(cudaEventCreateWithFlags(&c->ce_fork[d], cudaEventDisableTiming));
       }
     }
     // DCBS: TP and DP groups on NCCL; PP stays on the peer kernels
@@ -595,19 +598,19 @@ ppc_status_t ppc_impl_send_ex(ppc_comm_t* c, ppc_dir_t d, const void* buf, size_
     a.rec_src = c->rank;
     a.rec_dst = h.peer_out;
     CK(launch_ce_head(a, s));
-    CK(cudaEventRecord(c->ce_fork, s));
+    CK(cudaEventRecord(c->ce_fork[d], s));
     const int C = std::min<int>(c->cfg.channels, (int)n_chunks);
     for (int i = 0; i < C; ++i) {
       const uint32_t c0 = (uint32_t)((uint64_t)n_chunks * i / C);
       const uint32_t c1 = (uint32_t)((uint64_t)n_chunks * (i + 1) / C);
       const size_t off = (size_t)c0 * c->chunk;
       const size_t len = std::min<size_t>((size_t)c1 * c->chunk, bytes) - off;
-      CK(cudaStreamWaitEvent(c->ce[i], c->ce_fork, 0));
+      CK(cudaStreamWaitEvent(c->ce[d][i], c->ce_fork[d], 0));
       CK(cudaMemcpyAsync(dst + off, static_cast<const uint8_t*>(buf) + off, len,
-                         cudaMemcpyDeviceToDevice, c->ce[i]));
-      CK(launch_ce_flags(flags, c0, c1, seq, i == C - 1 ? rec : nullptr, c->ce[i]));
-      CK(cudaEventRecord(c->ce_join[i], c->ce[i]));
-      CK(cudaStreamWaitEvent(s, c->ce_join[i], 0));
+                         cudaMemcpyDeviceToDevice, c->ce[d][i]));
+      CK(launch_ce_flags(flags, c0, c1, seq, i == C - 1 ? rec : nullptr, c->ce[d][i]));
+      CK(cudaEventRecord(c->ce_join[d][i], c->ce[d][i]));
+      CK(cudaStreamWaitEvent(s, c->ce_join[d][i], 0));
     }
   }
   // zero-copy: the send completes when the receiver has pulled it (on s_wait)
@@ -1134,11 +1137,13 @@ ppc_status_t ppc_destroy(ppc_comm_t* c) {
       if (c->side[d]) cudaStreamDestroy(c->side[d]);
       if (c->zcw[d]) cudaStreamDestroy(c->zcw[d]);
     }
-    for (int i = 0; i < 8; ++i) {
-      if (c->ce[i]) cudaStreamDestroy(c->ce[i]);
-      if (c->ce_join[i]) cudaEventDestroy(c->ce_join[i]);
+    for (int d = 0; d < 2; ++d) {
+      for (int i = 0; i < 8; ++i) {
+        if (c->ce[d][i]) cudaStreamDestroy(c->ce[d][i]);
+        if (c->ce_join[d][i]) cudaEventDestroy(c->ce_join[d][i]);
+      }
+      if (c->ce_fork[d]) cudaEventDestroy(c->ce_fork[d]);
     }
-    if (c->ce_fork) cudaEventDestroy(c->ce_fork);
     if (c->trace_dev) cudaFree(c->trace_dev);
     for (int k = 0; k < 2; ++k)
       for (cudaEvent_t e : c->tev[k]) cudaEventDestroy(e);

@@ -160,8 +160,11 @@ struct ppc_comm {
   bool zc_side = false;                        // step driver publishes zero-copy on side[d]
   bool fuse_publish = true;                    // step driver: publish from the prior receive
   bool zc_stepbufs = true;                     // step driver buffers are zero-copy sources
-  cudaStream_t ce[8] = {};                     // CE engine channel streams
-  cudaEvent_t ce_fork = nullptr, ce_join[8] = {};
+  // CE engine channel streams, one set per direction: a middle stage's FWD and BWD copies
+  // must not queue behind each other (a FWD copy waiting for its credit would hold up the
+  // BWD copy the other neighbour needs — a false dependency the 1F1B order does not have)
+  cudaStream_t ce[2][8] = {};
+  cudaEvent_t ce_fork[2] = {}, ce_join[2][8] = {};
   ppc_record_t* trace_dev = nullptr;
   int trace_n = 0;
   // cfg.trace bit 1: event pairs around send (0) / recv (1) launches

@@ -32,8 +32,6 @@ ppc_status_t ensure_bufs(ppc_comm* c, size_t bytes) {
     CK(cudaEventCreateWithFlags(&sb.xdone, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&sb.dgo, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&sb.djoin, cudaEventDisableTiming));
-    CK(cudaStreamCreateWithFlags(&sb.ds, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&sb.hs, cudaStreamNonBlocking));
     for (int d = 0; d < 2; ++d) {
       CK(cudaEventCreateWithFlags(&sb.join[d], cudaEventDisableTiming));
       for (int i = 0; i < 2; ++i) {
@@ -199,6 +197,7 @@ struct Stepper {
   // 2 = obuf [d][bi], 0 = a caller buffer)
   ppc_status_t d2h(void* dst, const void* src, size_t bytes, int kind, int d, int bi) {
     StepBufs& sb = c->sb;
+    if (!sb.ds) CK(cudaStreamCreateWithFlags(&sb.ds, cudaStreamNonBlocking));   // first use
     CK(cudaEventRecord(sb.dgo, cs));
     CK(cudaStreamWaitEvent(sb.ds, sb.dgo, 0));
     CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, sb.ds));
@@ -349,6 +348,7 @@ struct Stepper {
             // staging buffer's previous contents are consumed (send done / copied by the next
             // virtual stage / read by this stage's fn / read by a device->host copy)
             uint8_t* r = sb.rbuf[d][bi];
+            if (!sb.hs) CK(cudaStreamCreateWithFlags(&sb.hs, cudaStreamNonBlocking));
             cudaStream_t q = sb.hs;
             if (dmode) {
               ppc_status_t e = PPC_OK;
@@ -479,6 +479,11 @@ struct Stepper {
           } else {
             // zero-copy: the buffer is free once consumed, awaited on zcw[d] off the
             // publication stream so the next publication is not queued behind it
+            if (zc_send && !zc_cs && !c->zcw[d]) {      // first zero-copy send off cs
+              int lo = 0, hi = 0;
+              cudaDeviceGetStreamPriorityRange(&lo, &hi);
+              CK(cudaStreamCreateWithPriority(&c->zcw[d], cudaStreamNonBlocking, hi));
+            }
             cudaStream_t s_pub = zc_cs ? cs : c->side[d];
             cudaStream_t s_done = zc_send ? (zc_cs ? c->side[d] : c->zcw[d]) : c->side[d];
             ppc_status_t ss = ppc_impl_send_ex(c, (ppc_dir_t)d, send_src, bytes, m, s_pub, s_done);
