@@ -3,6 +3,8 @@ D2H -> pinned /dev/shm ring -> H2D) and the device-direct path (libppc) deliver 
 messages — the delivery log (seq, mb, bytes, blake2b-128 digest) of every (boundary,
 direction) is identical for both and equal to the CPU oracle's (oracle/transfer.py via
 oracle/proxy.run_1f1b) on the same seeded inputs, and the delivered bytes are identical."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -20,7 +22,9 @@ def _b1_step(X, G, n, M, K, channels, chunk, tag):
     """One comm-only 1F1B step of a PP = 2 pipeline over B1, both stages in this process,
     stepped by one host thread in dependency order (a send never blocks on a full ring)."""
     s = torch.cuda.current_stream()
-    links = {name: CpuFwdLink(f"{name}_{tag}", snd, n, chunk, K, channels, 0)
+    # one shared ring per direction: the sender end creates "/ppcb_<dir>_<tag>", the
+    # receiver end opens the same name
+    links = {name: CpuFwdLink(f"{name[0]}_{tag}_{os.getpid()}", snd, n, chunk, K, channels, 0)
              for name, snd in (("fs", True), ("fr", False), ("bs", True), ("br", False))}
     for ln in links.values():
         ln.connect()
