@@ -872,6 +872,17 @@ ppc_status_t ppc_pp_recv_gather(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t to
   if (ppc_status_t ts = time_mark(c, 1, s, true)) return ts;
   CK(launch_gather(a, grid, s));
   if (ppc_status_t ts = time_mark(c, 1, s, false)) return ts;
+  // the credit waits for the OTHER receivers' pulls of our sender's slice: on the direction's
+  // side stream (after this gather), not on s
+  if (!c->gcw[d]) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    CK(cudaStreamCreateWithPriority(&c->gcw[d], cudaStreamNonBlocking, hi));
+  }
+  if (!c->g_ev[d]) CK(cudaEventCreateWithFlags(&c->g_ev[d], cudaEventDisableTiming));
+  CK(cudaEventRecord(c->g_ev[d], s));
+  CK(cudaStreamWaitEvent(c->gcw[d], c->g_ev[d], 0));
+  CK(launch_gather_credit(a, c->gcw[d]));
   h.recv_seq = seq;
   c->gcount[d] += 1;
   return PPC_OK;
@@ -1150,7 +1161,11 @@ ppc_status_t ppc_destroy(ppc_comm_t* c) {
     if (c->hx_buf) cudaFree(c->hx_buf);
     if (c->seg_tab) cudaFree(c->seg_tab);
     if (c->dseq) cudaFree(c->dseq);
-    for (int d = 0; d < 2; ++d) if (c->zc_ev[d]) cudaEventDestroy(c->zc_ev[d]);
+    for (int d = 0; d < 2; ++d) {
+      if (c->zc_ev[d]) cudaEventDestroy(c->zc_ev[d]);
+      if (c->g_ev[d]) cudaEventDestroy(c->g_ev[d]);
+      if (c->gcw[d]) cudaStreamDestroy(c->gcw[d]);
+    }
     if (c->arena) cudaFree(c->arena);
     if (c->err_host) cudaFreeHost(c->err_host);
     if (c->err_dev) cudaFree(c->err_dev);

@@ -156,6 +156,8 @@ struct ppc_comm {
   std::vector<int> members[3];
   cudaStream_t side[2] = {nullptr, nullptr};   // send streams of the step driver
   cudaStream_t zcw[2] = {nullptr, nullptr};    // step driver: zero-copy consumption waits
+  cudaStream_t gcw[2] = {nullptr, nullptr};    // TP-sliced gathers: credit releases
+  cudaEvent_t g_ev[2] = {nullptr, nullptr};
   bool step_inplace = false;                   // step driver: stage fns produce into the slot
   bool zc_side = false;                        // step driver publishes zero-copy on side[d]
   bool fuse_publish = true;                    // step driver: publish from the prior receive

@@ -154,6 +154,9 @@ struct GatherArgs {
   uint64_t timeout_ns;
 };
 cudaError_t launch_gather(const GatherArgs& a, int grid, cudaStream_t s);
+// the gather's credit: waits (1 thread, bounded) until every receiver pulled our sender's
+// slice, then releases the sender's credit; enqueued on a side stream after the gather
+cudaError_t launch_gather_credit(const GatherArgs& a, cudaStream_t s);
 
 
 // CE engine pieces: header/credit kernel before the copies, flag kernel after each.

@@ -887,14 +887,30 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(GatherArgs a) {
     *a.done = 0;
     __threadfence_system();
     for (uint32_t t = 0; t < a.tp; ++t) atomicAdd_system(a.gdone[t], 1ull);   // "pulled"
-    // our sender's slice may be reused once every receiver of the stage has pulled it
-    if (!wait_geq<true>(reinterpret_cast<const uint64_t*>(a.gdone[a.my_tp]), a.gtarget,
-                        globaltimer() + a.timeout_ns)) {
-      latch(a.err, PPC_ERR_TIMEOUT, a.seq, 0x600u);
-      return;
-    }
-    st_release_sys(a.peer_credit, a.seq);
+    // our sender's slice may be reused once EVERY receiver of the stage has pulled it: that
+    // wait (and the credit) is gather_credit_kernel's, on a side stream, so the next gather
+    // on this stream does not queue behind the slowest receiver
   }
+}
+
+// The credit of a TP-sliced gather: once every receiver of the stage counted its pull of our
+// sender's slice (gdone >= gtarget), release the sender's credit.  One thread, bounded.
+__global__ void gather_credit_kernel(const unsigned long long* gdone, uint64_t gtarget,
+                                     uint64_t* peer_credit, uint64_t seq, ErrWord* err,
+                                     uint64_t timeout_ns) {
+  pdl_enter();
+  if (!wait_geq<true>(reinterpret_cast<const uint64_t*>(gdone), gtarget,
+                      globaltimer() + timeout_ns)) {
+    latch(err, PPC_ERR_TIMEOUT, seq, 0x600u);
+    return;
+  }
+  st_release_sys(peer_credit, seq);
+}
+
+cudaError_t launch_gather_credit(const GatherArgs& a, cudaStream_t s) {
+  return launch_k(gather_credit_kernel, 1, 1, s, true,
+                  static_cast<const unsigned long long*>(a.gdone[a.my_tp]), a.gtarget,
+                  a.peer_credit, a.seq, a.err, a.timeout_ns);
 }
 
 cudaError_t launch_gather(const GatherArgs& a, int grid, cudaStream_t s) {
@@ -1210,6 +1226,7 @@ cudaError_t preload_kernels() {
       (const void*)recv_batch_kernel<true, false>, (const void*)recv_batch_kernel<false, false>,
       (const void*)recv_batch_kernel<true, true>, (const void*)recv_batch_kernel<false, true>,
       (const void*)gather_kernel,          (const void*)publish_kernel,
+      (const void*)gather_credit_kernel,
       (const void*)ce_head_kernel,         (const void*)ce_flags_kernel,
       (const void*)wait_credit_kernel,     (const void*)set_seq_kernel,
       (const void*)add_kernel<float>,      (const void*)add_kernel<__half>,
