@@ -21,7 +21,6 @@ struct ppc_graph {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   unsigned long long kernels = 0;                 // libppc kernel nodes (ppc_launch_count)
-  int pdl_edges = 0;                              // cross-stream edges made programmatic
 };
 
 namespace {
@@ -69,52 +68,6 @@ cudaEvent_t new_event() {
 }
 
 #define GDBG(...) do { if (getenv("PPC_DEBUG")) fprintf(stderr, __VA_ARGS__); } while (0)
-
-// Cross-stream dependencies of the captured step (a receiving stage's hand-off copy waits for
-// the other stage's copy) are full completion edges: the dependent kernel is launched only
-// after its predecessor finished, paying launch and CTA-rasterisation latency on the
-// critical path at every hand-off.  Kernels that begin with griddepcontrol.wait and never
-// spin (pdl_safe_kernel) can take PROGRAMMATIC edges instead — launched once the upstream
-// kernel triggered (right at its start), resident behind it, released by the hardware when
-// it completes with its memory visible — as same-stream PDL launches already are.
-// PPC_GRAPH_PDL=0 keeps the full edges.  Returns the number of converted edges.
-int programmatic_edges(cudaGraph_t graph) {
-  if (!env_int("PPC_GRAPH_PDL", 1)) return 0;
-  size_t n = 0;
-  if (cudaGraphGetEdges_v2(graph, nullptr, nullptr, nullptr, &n) != cudaSuccess || n == 0) {
-    cudaGetLastError();
-    return 0;
-  }
-  std::vector<cudaGraphNode_t> from(n), to(n);
-  std::vector<cudaGraphEdgeData> ed(n);
-  if (cudaGraphGetEdges_v2(graph, from.data(), to.data(), ed.data(), &n) != cudaSuccess) {
-    cudaGetLastError();
-    return 0;
-  }
-  int converted = 0;
-  for (size_t i = 0; i < n; ++i) {
-    if (ed[i].type != cudaGraphDependencyTypeDefault || ed[i].from_port != 0) continue;
-    cudaGraphNodeType tf, tt;
-    if (cudaGraphNodeGetType(from[i], &tf) != cudaSuccess ||
-        cudaGraphNodeGetType(to[i], &tt) != cudaSuccess || tf != cudaGraphNodeTypeKernel ||
-        tt != cudaGraphNodeTypeKernel)
-      continue;
-    cudaKernelNodeParams kp{};
-    if (cudaGraphKernelNodeGetParams(to[i], &kp) != cudaSuccess || !pdl_safe_kernel(kp.func))
-      continue;
-    cudaGraphEdgeData pe{};
-    pe.from_port = cudaGraphKernelNodePortProgrammatic;
-    pe.type = cudaGraphDependencyTypeProgrammatic;
-    if (cudaGraphRemoveDependencies_v2(graph, &from[i], &to[i], &ed[i], 1) != cudaSuccess) break;
-    if (cudaGraphAddDependencies_v2(graph, &from[i], &to[i], &pe, 1) != cudaSuccess) {
-      cudaGraphAddDependencies_v2(graph, &from[i], &to[i], &ed[i], 1);   // restore
-      break;
-    }
-    ++converted;
-  }
-  cudaGetLastError();
-  return converted;
-}
 
 }  // namespace
 
@@ -219,7 +172,6 @@ ppc_status_t ppc_graph_create(ppc_comm_t* const* comms, int n, const ppc_step_t*
   if (fork) cudaEventDestroy(fork);
   for (cudaEvent_t j : joins) if (j) cudaEventDestroy(j);
   st = finish(st);
-  if (!st && graph) g->pdl_edges = programmatic_edges(graph);
   g->kernels = g_launches.load() - launches0;   // captured, not run: counted per replay
   g_launches.fetch_sub(g->kernels);
   g->graph = graph;

@@ -194,8 +194,6 @@ cudaError_t launch_add(void* dst, const void* src, size_t count, int dtype, cuda
 // Same-GPU single copy (direct mode of virtual stages): dst <- src, `bytes`, CTA chunks.
 cudaError_t launch_copy(void* dst, const void* src, uint64_t bytes, uint64_t chunk, int grid,
                         cudaStream_t s);
-// kernels that may take a programmatic (PDL) graph edge from any upstream kernel
-bool pdl_safe_kernel(const void* func);
 // load every transport kernel on the current device now (see ppc_kernels.cu)
 cudaError_t preload_kernels();
 // launch transport kernels with programmatic dependent launch (ppc_kernels.cu); set from

@@ -1117,12 +1117,6 @@ __global__ void __launch_bounds__(32) copy_tma_kernel(uint8_t* dst, const uint8_
 }
 
 
-bool pdl_safe_kernel(const void* func) {
-  // begins with griddepcontrol.wait, never waits on another kernel: may take a programmatic
-  // graph edge (ppc_graph.cu)
-  return func == (const void*)copy_kernel || func == (const void*)copy_tma_kernel;
-}
-
 cudaError_t launch_copy(void* dst, const void* src, uint64_t bytes, uint64_t chunk, int grid,
                         cudaStream_t s) {
   if (bytes == 0) return cudaSuccess;
