@@ -324,9 +324,13 @@ class Ctx:
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.distributed = self.world > 1
         if self.distributed:
-            torch.cuda.set_device(self.local)
+            # one GPU per rank; with fewer GPUs than ranks (a rehearsal of the 8-GPU path on a
+            # 4-GPU box) ranks share GPUs round-robin — the numbers are then not a bench line
+            self.shared_gpus = self.world > torch.cuda.device_count()
+            torch.cuda.set_device(self.local % torch.cuda.device_count())
             dist.init_process_group("gloo")
         else:
+            self.shared_gpus = False
             torch.cuda.set_device(0)
         self.dev = torch.cuda.current_device()
 
@@ -368,7 +372,7 @@ class Pipeline:
                               chunk_bytes=wl["chunk"], engine=engine,
                               cta_per_channel=wl["cta"], trace=3)
         if ctx.distributed:
-            self.comms = [ppc.connect_distributed(cfg, ctx.rank, ctx.world, ctx.local,
+            self.comms = [ppc.connect_distributed(cfg, ctx.rank, ctx.world, ctx.dev,
                                                   with_nccl=wl["tp"] > 1)]
             self.stages = [self.comms[0].group(ppc.GROUP_PP)[0].index(ctx.rank)]
         else:
@@ -819,6 +823,9 @@ def main():
             line["intra_device_ring"] = ring
         if extra:
             line["north_star_configs"] = extra
+        if ctx.shared_gpus:
+            line["shared_gpus"] = ("REHEARSAL: more ranks than GPUs, ranks share GPUs "
+                                   "(time-sliced); not a bench line")
         if ctx.distributed and wl["pp"] == 2:
             t_msg = wl["msg_bytes"] / (NVLINK_GBPS * 1e3)
             line["step_roofline"] = {"us": (wl["M"] + 1) * t_msg,
