@@ -589,6 +589,13 @@ def e2e_leg(ctx, p, wl, steps):
             "roofline": pcie_roofline(ctx.world, h2d / ctx.world, d2h / ctx.world, ms / K2)}
 
 
+def b1_pair(rank, world):
+    """(stage, rank of the pipeline's stage-0 rank) of `rank` in a PP = 2, TP = 1 grid of
+    `world` ranks: rank = pp_i * dp + dp_i (S:L479), so stage = rank // dp, pipeline = dp_i."""
+    dp = world // 2
+    return rank // dp, rank % dp
+
+
 def b1_arm(ctx, wl, steps=3, channels=4, chunk=4 << 20):
     """CPU-Forwarding baseline B1 (libppcb, P:L37/P:L47/P:L163): D2H into a pinned /dev/shm
     ring, per-chunk host flags, H2D at the receiver, `channels` host threads — the same
@@ -613,9 +620,8 @@ def b1_arm(ctx, wl, steps=3, channels=4, chunk=4 << 20):
     if ctx.distributed:
         pids = [None] * ctx.world
         ctx.dist.all_gather_object(pids, os.getpid())
-        dpw = ctx.world // 2                    # rank = pp_i * dp + dp_i (pp = 2, tp = 1)
-        st = ctx.rank // dpw                    # stage of this rank; its pipeline = dp_i
-        lead = pids[ctx.rank % dpw]
+        st, lead_rank = b1_pair(ctx.rank, ctx.world)
+        lead = pids[lead_rank]
         fwd = CpuFwdLink(f"b1f_{lead}", st == 0, nb, chunk, K, channels, dev)
         bwd = CpuFwdLink(f"b1b_{lead}", st == 1, nb, chunk, K, channels, dev)
         ctx.dist.barrier()
@@ -678,7 +684,7 @@ def b1_arm(ctx, wl, steps=3, channels=4, chunk=4 << 20):
     torch.cuda.synchronize()
     dt = ctx.max_over_ranks(time.perf_counter() - t0)
     ok = True
-    st_here = [0, 1] if not ctx.distributed else [ctx.rank // (ctx.world // 2)]
+    st_here = [0, 1] if not ctx.distributed else [b1_pair(ctx.rank, ctx.world)[0]]
     for m in range(M):
         if 1 in st_here:
             ok &= bool(torch.equal(OUT[1][m], X[m]))

@@ -811,11 +811,11 @@ ppc_status_t ppc_pp_recv_batch(ppc_comm_t* c, ppc_dir_t d, void* const* bufs,
   if (n < 1 || n > kMaxBatch || !bufs || !bytes || mb0 < 0) return PPC_ERR_INVALID_ARG;
   Chan& h = c->ch[d];
   if (h.peer_in < 0) return PPC_ERR_NO_NEIGHBOR;
-  if (c->device < 0) return PPC_ERR_STATE;
   for (int i = 0; i < n; ++i) {        // every argument error before anything is enqueued
     if (bytes[i] > 0 && !bufs[i]) return PPC_ERR_INVALID_ARG;
     if (bytes[i] > c->cfg.max_msg_bytes) return PPC_ERR_TOO_LARGE;
   }
+  if (c->device < 0) return PPC_ERR_STATE;
   if (c->local_mode && h.in_comm->ch[d].send_seq < h.recv_seq + n) return PPC_ERR_WOULD_BLOCK;
   DeviceGuard g(c->device);
   RecvArgs as[kMaxBatch];

@@ -107,6 +107,19 @@ def test_host_only_data_path_is_state_error():
     assert begin(comms[0].h, ppc.FWD, 16, 0, None, sl) == ppc.STATUS.index("STATE")  # no device
     assert end(comms[0].h, ppc.FWD, 0, None) == ppc.STATUS.index("STATE")     # nothing open
     assert end(comms[0].h, 7, 0, None) == ppc.STATUS.index("INVALID_ARG")
+    # batched receive: argument errors before anything is enqueued
+    rb = ppc._recv_batch
+    bufs = (ctypes.c_void_p * 17)(*([0x1000] * 17))
+    sizes = (ctypes.c_size_t * 17)(*([16] * 17))
+    big = (ctypes.c_size_t * 2)(16, 64 << 20)
+    nul = (ctypes.c_void_p * 2)(0x1000, 0)
+    assert rb(comms[1].h, ppc.FWD, bufs, sizes, 0, 0, None) == ppc.STATUS.index("INVALID_ARG")
+    assert rb(comms[1].h, ppc.FWD, bufs, sizes, 17, 0, None) == ppc.STATUS.index("INVALID_ARG")
+    assert rb(comms[1].h, ppc.FWD, bufs, sizes, 2, -1, None) == ppc.STATUS.index("INVALID_ARG")
+    assert rb(comms[1].h, ppc.FWD, nul, sizes, 2, 0, None) == ppc.STATUS.index("INVALID_ARG")
+    assert rb(comms[1].h, ppc.FWD, bufs, big, 2, 0, None) == ppc.STATUS.index("TOO_LARGE")
+    assert rb(comms[0].h, ppc.FWD, bufs, sizes, 2, 0, None) == ppc.STATUS.index("NO_NEIGHBOR")
+    assert rb(comms[1].h, ppc.FWD, bufs, sizes, 2, 0, None) == ppc.STATUS.index("STATE")
     for c in comms:
         c.destroy()
 
@@ -128,4 +141,17 @@ def test_connect_rejects_bad_blobs():
         a.connect([ba, other.export()])
     assert e.value.name == "INVALID_ARG"
     for c in (a, b, other):
+        c.destroy()
+
+
+def test_launch_counter_is_monotone():
+    a = ppc.launch_count()
+    assert a >= 0 and ppc.launch_count() >= a
+
+
+def test_config_local_spin_field():
+    cfg = ppc.make_config(pp=3, local_spin=1)
+    assert cfg.local_spin == 1 and cfg.pp == 3
+    comms = [ppc.Comm(cfg, 3, r, -1) for r in range(3)]     # host-only: accepted, no device
+    for c in comms:
         c.destroy()
