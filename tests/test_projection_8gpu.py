@@ -62,3 +62,27 @@ def test_project_c3_c4_8gpu():
     print(json.dumps({"projection": out, "pp4_calibration_factor": bias,
                       "inputs": {k: m[k] for k in ("link_gbps", "per_message_overhead_us")}},
                      indent=1))
+
+
+def test_project_c4_exposure_with_compute():
+    """Exposed PP comm of C4 (Qwen2-7B, PP8, M32) with stage compute, projected: per-stage
+    compute = its MLP blocks (28 over 8 stages: 4,4,4,4,3,3,3,3) at the per-block time
+    measured for the LLaMA block (profiles/round2/pc8_partition_sustained.jsonl: stage 1,
+    sustained clocks) scaled by the Qwen/LLaMA block FLOP ratio; messages 28 MiB at the
+    measured rate and per-message overhead.  exposed = (T - T_no_comm) / T."""
+    m = _load()
+    with open(os.path.join(os.path.dirname(RATES), "pc8_partition_sustained.jsonl")) as fh:
+        rec = json.loads(fh.readline())
+    t_llama = rec["planner"]["t_fwd_ms"][1] * 1e3                 # us per block, fwd
+    ratio = (3584 * 18944) / (4096 * 14336)                       # MLP FLOPs per token
+    blocks = [4, 4, 4, 4, 3, 3, 3, 3]
+    f = lambda s_, m_: blocks[s_] * t_llama * ratio
+    b = lambda s_, m_: 2 * f(s_, m_)
+    nbytes = 4096 * 3584 * 2
+    link = LinkModel(bw=m["link_gbps"] * 1e3, latency=m["per_message_overhead_us"], mode="shared")
+    t = simulate(8, 32, f, b, nbytes, nbytes, link, K=9).makespan
+    t0 = simulate(8, 32, f, b, 0, 0, LinkModel(bw=1.0), K=9).makespan
+    exposed = (t - t0) / t
+    print(json.dumps({"projection": {"C4 exposed PP comm with MLP compute": exposed,
+                                     "step_ms": t / 1e3, "step_ms_no_comm": t0 / 1e3}}))
+    assert 0.0 <= exposed < 0.05                                 # the BASELINE target
