@@ -839,44 +839,48 @@ cudaError_t launch_recv_batch(const RecvBatch& b, int grid, bool sys, cudaStream
 __global__ void __launch_bounds__(kThreads) gather_kernel(GatherArgs a) {
   pdl_enter();
   __shared__ const uint8_t* s_src[kMaxTp];
-  uint64_t deadline = 0;
-  int fail = 0;
-  if (threadIdx.x == 0) {
-    deadline = globaltimer() + a.timeout_ns;
-    for (uint32_t t = 0; t < a.tp && !fail; ++t) {
-      if (!wait_geq<true>(a.hdr_flag[t], a.seq, deadline)) {
-        latch(a.err, PPC_ERR_TIMEOUT, a.seq, 0x400u | t << 12);
-        fail = 1;
-        break;
-      }
-      const volatile SlotHeader* h = a.hdr[t];
-      if (h->magic != kMagic || h->seq != a.seq || h->mb != a.mb || !(h->flags & kHdrZeroCopy)) {
-        latch(a.err, PPC_ERR_ORDER, a.seq, 0x400u | t << 12);
-        fail = 1;
-      } else if (h->bytes != a.slice_bytes) {
-        latch(a.err, PPC_ERR_SIZE_MISMATCH, a.seq, 0x400u | t << 12);
-        fail = 1;
-      } else {
-        const uint32_t seg = h->src_seg;
-        const uint64_t base = seg < (uint32_t)kMaxSeg ? a.seg_tab[t][seg] : 0;
-        if (!base) {
-          latch(a.err, PPC_ERR_ORDER, a.seq, 0x500u | t << 12);
-          fail = 1;
-        } else {
-          s_src[t] = reinterpret_cast<const uint8_t*>(base + h->src_off);
-        }
-      }
-    }
-  }
-  if (__syncthreads_or(fail)) return;
+  const uint64_t deadline = globaltimer() + a.timeout_ns;
+  if (threadIdx.x == 0)
+    for (uint32_t t = 0; t < a.tp; ++t) s_src[t] = nullptr;
+  __syncthreads();
   // every CTA pulls (slice, chunk) units of all TP senders over NVLink into its slot of dst.
   // Units interleave the senders (consecutive units come from different senders) and each
   // receiver starts at its own TP index, so at any time a receiver pulls from every sender
   // and every sender serves every receiver — not all receivers draining sender 0 first
-  // (measured: 322 GB/s per receiver sender-major vs the replicated boundary's 607)
+  // (measured: 322 GB/s per receiver sender-major vs the replicated boundary's 607).  A
+  // sender's header (published in that sender's PP peer's arena) is acquired when the CTA
+  // first needs a unit of it, so pulling from the own sender (header in our arena) starts
+  // before the other senders' publications are seen.
   const uint32_t units = a.tp * a.n_chunks;
   for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
     const uint32_t t = (u + a.my_tp) % a.tp, c = u / a.tp;
+    if (!s_src[t]) {
+      int fail = 0;
+      if (threadIdx.x == 0) {
+        if (!wait_geq<true>(a.hdr_flag[t], a.seq, deadline)) {
+          latch(a.err, PPC_ERR_TIMEOUT, a.seq, 0x400u | t << 12);
+          fail = 1;
+        } else {
+          const HdrView h = read_header(a.hdr[t]);
+          if (h.magic != kMagic || h.seq != a.seq || h.mb != a.mb || !(h.flags & kHdrZeroCopy)) {
+            latch(a.err, PPC_ERR_ORDER, a.seq, 0x400u | t << 12);
+            fail = 1;
+          } else if (h.bytes != a.slice_bytes) {
+            latch(a.err, PPC_ERR_SIZE_MISMATCH, a.seq, 0x400u | t << 12);
+            fail = 1;
+          } else {
+            const uint64_t base = h.src_seg < (uint32_t)kMaxSeg ? a.seg_tab[t][h.src_seg] : 0;
+            if (!base) {
+              latch(a.err, PPC_ERR_ORDER, a.seq, 0x500u | t << 12);
+              fail = 1;
+            } else {
+              s_src[t] = reinterpret_cast<const uint8_t*>(base + h.src_off);
+            }
+          }
+        }
+      }
+      if (__syncthreads_or(fail)) return;
+    }
     const uint64_t off = (uint64_t)c * a.chunk;
     const uint64_t len = min(a.chunk, a.slice_bytes - off);
     cta_copy<true>(a.dst + (uint64_t)t * a.slice_bytes + off, s_src[t] + off, len);
