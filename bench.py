@@ -589,6 +589,57 @@ def e2e_leg(ctx, p, wl, steps):
             "roofline": pcie_roofline(ctx.world, h2d / ctx.world, d2h / ctx.world, ms / K2)}
 
 
+def p2p_stream_leg(ctx, n=64 << 20, N=16, reps=5):
+    """The metric's first half, "stage-boundary P2P GB/s vs NVLink" (BJ target: >= 80 % of
+    900 GB/s for messages >= 64 MB): every pipeline's stage 0 streams N messages of n bytes
+    to its stage 1 — zero-copy publications (cfg.zc_async) from a registered buffer, one
+    batched receive grid for all N (ppc_pp_recv_batch) — timed on the sender's stream from
+    the first publication to ppc_pp_wait_consumed (every byte in the receiver's buffers);
+    median of `reps`, max over ranks of the time.  PP = 2 pairs only."""
+    torch, ppc = ctx.torch, ctx.ppc
+    st, _ = b1_pair(ctx.rank, ctx.world)
+    cfg = ppc.make_config(pp=2, dp=ctx.world // 2, max_msg_bytes=n, chunk_bytes=256 << 10,
+                          zc_async=1)
+    comm = ppc.connect_distributed(cfg, ctx.rank, ctx.world, ctx.dev, with_nccl=False)
+    src = torch.empty(n, dtype=torch.uint8, device=ctx.dev)
+    ppc.fill_payload(src, n, 42, 0, 0, 0, 0)
+    torch.cuda.synchronize()
+    ppc.register_tensors(comm, [src] if st == 0 else [])
+    dsts = [torch.empty(n, dtype=torch.uint8, device=ctx.dev) for _ in range(N)] if st == 1 else []
+    s = torch.cuda.Stream()
+    times, mb = [], 0
+    for rep in range(reps + 1):
+        ctx.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        if st == 0:
+            for i in range(N):
+                comm.send(ppc.FWD, src, n, mb=mb + i, stream=s)
+            comm.wait_consumed(ppc.FWD, s)
+        else:
+            comm.recv_batch(ppc.FWD, dsts, n, mb0=mb, stream=s)
+        e1.record(s)
+        mb += N
+        ctx.barrier()
+        t = ctx.max_over_ranks(e0.elapsed_time(e1) if st == 0 else 0.0)
+        if rep:
+            times.append(t)
+    # every rank filled `src` with the same payload: each received buffer must equal it
+    ok = all(bool(torch.equal(d, src)) for d in dsts)
+    ok = ctx.all_true(ok and comm.poll() == 0)
+    ctx.barrier()
+    comm.disconnect()
+    ctx.dist.barrier()
+    comm.destroy()
+    t = statistics.median(times) * 1e-3
+    gbps = N * n / t / 1e9
+    return {"bytes": n, "messages": N, "gbps_per_direction": gbps, "frac_of_900": gbps / NVLINK_GBPS,
+            "target": ">= 0.80 of 900 GB/s for >= 64 MB (BASELINE.json)", "outputs_checked": ok,
+            "how": "zero-copy publications (zc_async) + one batched receive grid per N messages, "
+                   "sender-stream CUDA events to ppc_pp_wait_consumed, median of "
+                   f"{reps}, max over ranks"}
+
+
 def b1_pair(rank, world):
     """(stage, rank of the pipeline's stage-0 rank) of `rank` in a PP = 2, TP = 1 grid of
     `world` ranks: rank = pp_i * dp + dp_i (S:L479), so stage = rank // dp, pipeline = dp_i."""
@@ -799,6 +850,14 @@ def main():
             r["config"] = config_dict(wx, ctx.world)
             extra[name] = r
 
+    # ---- stage-boundary P2P GB/s (the metric's first half), N >= 2
+    p2p = None
+    if ctx.distributed and not ctx.shared_gpus and ctx.world % 2 == 0:
+        try:
+            p2p = p2p_stream_leg(ctx)
+        except Exception as e:
+            p2p = {"error": repr(e)[:200]}
+
     # ---- CPU-Forwarding B1 on the headline workload
     b1 = None
     if not args.no_b1:
@@ -827,6 +886,8 @@ def main():
             line["device_direct_vs_cpu_forwarding"] = value / b1["value"]
         if ring:
             line["intra_device_ring"] = ring
+        if p2p:
+            line["p2p_stream_64MiB"] = p2p
         if extra:
             line["north_star_configs"] = extra
         if ctx.shared_gpus:
