@@ -666,3 +666,59 @@ def test_mpdt_channels(C, mode):
     for (d, i), t in outs.items():
         assert np.array_equal(_host(t)[:sizes[i]], P.payload_bytes(42, 0, 0, d, i, sizes[i])), (d, i)
     _close(comms)
+
+
+@pytest.mark.parametrize("name", ["C4", "C3"])
+def test_full_size_north_star_configs_on_one_gpu(name):
+    """BASELINE configs[3] C4 (Qwen2-7B [1,4096,3584] bf16, PP = 8, M = 32) and configs[2] C3
+    (LLaMA-8B [1,4096,4096], PP = 4 x TP = 2: two TP pipelines, M = 16) at full size with
+    bench.py's launch configuration for them (ring push, 512 KiB chunks, K = pp + 1) — every
+    rank a comm of this process on one GPU
+    under the cross-process protocol.  Identity stages: every Y_m of the last stages equals
+    the stage-0 input X_m and every DX_m of stage 0 equals G_m, checked for ALL micro-batches
+    against the synth payloads by digest (plus first / last bytes)."""
+    import bench
+    a = bench.parse([])
+    wl = bench.resolve(a, 8, name)
+    S, TP, M, n = wl["pp"], wl["tp"], wl["M"], wl["msg_bytes"]
+    comms = _comms(tp=TP, pp=S, max_msg_bytes=n, chunk_bytes=wl["chunk"], ring_slots=wl["slots"])
+    world = len(comms)
+    dig = lambda x: hashlib.blake2b(x.tobytes(), digest_size=16).digest()
+    ref_x = [P.source_activation(42, 0, m, n) for m in range(M)]
+    ref_g = [P.source_gradient(42, 0, m, n) for m in range(M)]
+    dx, dg = [dig(x) for x in ref_x], [dig(g) for g in ref_g]
+    X = [_buf(n) for _ in range(M)]
+    G = [_buf(n) for _ in range(M)]
+    for m in range(M):
+        ppc.fill_payload(X[m], n, 42, 0, P.SRC_BOUNDARY, 0, m)
+        ppc.fill_payload(G[m], n, 42, 0, P.SRC_BOUNDARY, 1, m)
+    outs = {}
+    args = []
+    for r, c in enumerate(comms):
+        st = c.group(ppc.GROUP_PP)[0].index(r)
+        y = [_buf(n) for _ in range(M)] if st == S - 1 else None
+        d = [_buf(n) for _ in range(M)] if st == 0 else None
+        outs[r] = (y, d)
+        args.append(ppc.StepArgs(M, n, n, x=X if st == 0 else None, g=G if st == S - 1 else None,
+                                 y=y, dx=d))
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    # eager steps (8 ranks' graphs would add 8 capture streams: this process must stay under
+    # the GPU's 32 hardware queues, DESIGN.md §6b); the second step runs on allocated buffers
+    # with continuing sequence numbers
+    for _ in range(2):
+        _step_all(comms, args, streams)
+        torch.cuda.synchronize()
+    for c in comms:
+        assert c.poll() == 0, c.error_info()
+    checked = 0
+    for r, (y, d) in outs.items():
+        for bufs, want, ref in ((y, dx, ref_x), (d, dg, ref_g)):
+            if bufs is None:
+                continue
+            for m in range(M):
+                h = _host(bufs[m])
+                assert dig(h) == want[m] and np.array_equal(h[:4096], ref[m][:4096]), (r, m)
+                checked += 1
+    assert checked == 2 * TP * M
+    _close(comms)
