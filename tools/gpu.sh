@@ -36,10 +36,10 @@ for step in "$@"; do
     ref)      timeout 600 python bench.py --impl reference > "$log" 2>&1 ;;
     launches) timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
                 --log-file gpurun_out/${TAG}_launches_n1.csv python bench.py --steps 2 --warmup 3 \
-                --no-e2e --no-cpu-baseline > "$log" 2>&1 ;;
+                --no-e2e --no-cpu-baseline --no-b1 --no-ring > "$log" 2>&1 ;;
     ncu)      timeout 900 ncu --set full --clock-control none --import-source on -k "regex:$arg" \
                 -s 4 -c 1 -o gpurun_out/${TAG}_prof_$(echo "$arg" | tr -c 'A-Za-z0-9\n' '_') \
-                python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > "$log" 2>&1 ;;
+                python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-b1 --no-ring > "$log" 2>&1 ;;
     py)       timeout 1200 python ${arg//,/ } > "$log" 2>&1 ;;
     trun)     PORT=$((PORT+1)); n=${arg%%,*}; rest=${arg#*,}
               timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node "$n" \
