@@ -122,6 +122,8 @@ _err_info = _sig("ppc_error_info", _i, [_vp, C.POINTER(C.c_uint), C.POINTER(C.c_
 _trace = _sig("ppc_trace", _i, [_vp, C.POINTER(Record), C.POINTER(_i)])
 _ktimes = _sig("ppc_kernel_times", _i, [_vp, _i, C.POINTER(C.c_float), C.POINTER(_i)])
 _set_trace = _sig("ppc_set_trace", _i, [_vp, _i])
+_dbg_stamps = _sig("ppc_debug_stamps", _i, [_vp, C.POINTER(C.c_ulonglong), C.POINTER(_ll),
+                                            C.POINTER(_i)])
 _disconnect = _sig("ppc_disconnect", _i, [_vp])
 _destroy = _sig("ppc_destroy", _i, [_vp])
 _status_str = _sig("ppc_status_str", C.c_char_p, [_i])
@@ -321,6 +323,19 @@ class Comm:
         n = C.c_int(cap)
         _check(_ktimes(self.h, kind, out, C.byref(n)), "ppc_kernel_times")
         return list(out[:n.value])
+
+    def debug_stamps(self, cap=4096):
+        """PPC_DBG_STAMPS receive-kernel stamps: list of (seq, dir, grid, [[4 stamps] per CTA])."""
+        st = (C.c_ulonglong * (cap * 512))()
+        meta = (C.c_longlong * (cap * 3))()
+        n = C.c_int(cap)
+        _check(_dbg_stamps(self.h, st, meta, C.byref(n)), "ppc_debug_stamps")
+        out = []
+        for i in range(n.value):
+            g = meta[3 * i + 2]
+            rows = [list(st[i * 512 + 4 * b: i * 512 + 4 * b + 4]) for b in range(g)]
+            out.append((meta[3 * i], meta[3 * i + 1], g, rows))
+        return out
 
     def trace(self, cap=8192):
         recs = (Record * cap)()

@@ -221,6 +221,11 @@ ppc_status_t ppc_create(const ppc_config_t* cfg, int world, int rank, int cuda_d
     // aliased streams add false dependencies behind spinning kernels
     if (cfg->trace && cudaMalloc(&c->trace_dev, sizeof(ppc_record_t) * kTraceCap) != cudaSuccess)
       return fail(PPC_ERR_CUDA);
+    if (env_int("PPC_DBG_STAMPS", 0)) {
+      const size_t nb = sizeof(uint64_t) * 4 * kDbgCtas * kDbgLaunches;
+      if (cudaMalloc(&c->dbg, nb) != cudaSuccess || cudaMemset(c->dbg, 0, nb) != cudaSuccess)
+        return fail(PPC_ERR_CUDA);
+    }
     if (cudaDeviceSynchronize() != cudaSuccess) return fail(PPC_ERR_CUDA);
     b.arena_ptr = (uint64_t)(uintptr_t)c->arena;
     b.has_arena = 1;
@@ -762,6 +767,12 @@ ppc_status_t ppc_impl_recv_prepare(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t
     a.flags = h.i_flags;
     a.done = h.i_done;
   }
+  if (c->dbg && !c->capturing && c->dbg_meta.size() / 3 < (size_t)kDbgLaunches) {
+    a.dbg = c->dbg + (c->dbg_meta.size() / 3) * 4 * kDbgCtas;
+    c->dbg_meta.push_back((long long)seq);
+    c->dbg_meta.push_back(d);
+    c->dbg_meta.push_back(std::min<long long>(recv_grid(c, n_chunks) + (pub ? 1 : 0), kDbgCtas));
+  }
   h.recv_seq = seq;
   return PPC_OK;
 }
@@ -1072,6 +1083,21 @@ ppc_status_t ppc_trace(ppc_comm_t* c, ppc_record_t* out, int* n) {
   return PPC_OK;
 }
 
+ppc_status_t ppc_debug_stamps(ppc_comm_t* c, unsigned long long* stamps, long long* meta,
+                              int* n) {
+  if (!c || !n || (*n > 0 && (!stamps || !meta))) return PPC_ERR_INVALID_ARG;
+  if (!c->dbg) { *n = 0; return PPC_OK; }
+  DeviceGuard g(c->device);
+  CK(cudaDeviceSynchronize());
+  const int k = std::min(*n, (int)(c->dbg_meta.size() / 3));
+  if (k > 0) {
+    CK(cudaMemcpy(stamps, c->dbg, sizeof(uint64_t) * 4 * kDbgCtas * k, cudaMemcpyDeviceToHost));
+    std::copy(c->dbg_meta.begin(), c->dbg_meta.begin() + 3 * k, meta);
+  }
+  *n = k;
+  return PPC_OK;
+}
+
 ppc_status_t ppc_kernel_times(ppc_comm_t* c, int kind, float* ms, int* n) {
   if (!c || !n || (kind != 0 && kind != 1) || (*n > 0 && !ms)) return PPC_ERR_INVALID_ARG;
   if (c->device < 0) { *n = 0; return PPC_OK; }
@@ -1156,6 +1182,7 @@ ppc_status_t ppc_destroy(ppc_comm_t* c) {
       if (c->ce_fork[d]) cudaEventDestroy(c->ce_fork[d]);
     }
     if (c->trace_dev) cudaFree(c->trace_dev);
+    if (c->dbg) cudaFree(c->dbg);
     for (int k = 0; k < 2; ++k)
       for (cudaEvent_t e : c->tev[k]) cudaEventDestroy(e);
     if (c->hx_buf) cudaFree(c->hx_buf);

@@ -22,6 +22,8 @@ constexpr uint32_t kBlobMagic = 0x50504342u;   // "BCPP"
 constexpr uint32_t kBlobVersion = 1;
 constexpr size_t kAlign = 4096;
 constexpr int kTraceCap = 8192;
+constexpr int kDbgCtas = 128;      // PPC_DBG_STAMPS: stamp rows per receive launch
+constexpr int kDbgLaunches = 4096;
 
 inline size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -190,6 +192,10 @@ struct ppc_comm {
   bool capturing = false;
   uint64_t cap_send[2] = {0, 0}, cap_recv[2] = {0, 0};
   uint64_t* dseq = nullptr;
+  // PPC_DBG_STAMPS: recv_kernel per-CTA stamps, kDbgCtas x 4 per launch, and per launch
+  // (seq, dir, grid) on the host
+  uint64_t* dbg = nullptr;
+  std::vector<long long> dbg_meta;
   Blob blob{};
 };
 

@@ -119,6 +119,7 @@ struct RecvArgs {
   const uint64_t* seg_tab;      // zero-copy: mapped bases of the sender's registered buffers
   const uint8_t* peer_arena;    // zero-copy from the sender's arena (src_seg == kArenaSeg)
   uint32_t channels;            // MPDT channels of the pulling / copy-out CTAs
+  uint64_t* dbg;                // PPC_DBG_STAMPS: 4 %globaltimer stamps per CTA, or nullptr
   // fused publication (step driver): when has_pub, the last CTA publishes `pub` (the next
   // op's zero-copy send) right after releasing this receive's credit
   uint32_t has_pub;

@@ -634,6 +634,10 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(const __grid_constant__ 
     }
   }
   pdl_enter();
+  // PPC_DBG_STAMPS (diagnostics): per CTA [0] released by griddepcontrol.wait, [1] header
+  // seen, [2] first chunk moved, [3] done
+  uint64_t* const dbg = a0.dbg ? a0.dbg + 4 * blockIdx.x : nullptr;
+  if (dbg && threadIdx.x == 0) dbg[0] = globaltimer();
   const RecvArgs a = resolve(a0);
   uint64_t deadline = 0;
   int fail = 0;
@@ -682,6 +686,7 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(const __grid_constant__ 
     }
   }
   if (__syncthreads_or(fail)) return;
+  if (dbg && threadIdx.x == 0) dbg[1] = globaltimer();
   const uint8_t* zc_src = s_zc_src;
   // the early pull is valid only for the message resolved now (CTA-uniform condition)
   const bool use_pre = kEarly && pre_ok && zc_src == s_early_src && s_early_seq == a.seq;
@@ -703,6 +708,7 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(const __grid_constant__ 
         skip = (uint64_t)kEarlyV * kThreads * sizeof(V32);
       }
       cta_copy<true>(a.dst + off + skip, zc_src + off + skip, len - skip);
+      if (dbg && threadIdx.x == 0 && c == it.first) dbg[2] = globaltimer();
       continue;
     }
     int f = 0;
@@ -715,6 +721,7 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(const __grid_constant__ 
   }
   __threadfence();                 // slot reads + user-buffer writes before the credit
   __syncthreads();
+  if (dbg && threadIdx.x == 0) dbg[3] = globaltimer();
   if (threadIdx.x == 0) {
     if (atomicAdd(a.done, 1u) == gridDim.x - 1) {
       *a.done = 0;                 // next use of this slot is stream-ordered after us
