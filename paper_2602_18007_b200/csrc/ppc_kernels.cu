@@ -759,6 +759,8 @@ __global__ void __launch_bounds__(kThreads) recv_batch_kernel(const __grid_const
   const uint32_t workers = gridDim.x - w0;
   for (uint32_t i = 0; i < b.n; ++i) {
     const RecvArgs a = resolve(b.a[i]);
+    uint64_t* const dbg = a.dbg ? a.dbg + 4 * blockIdx.x : nullptr;   // PPC_DBG_STAMPS
+    if (dbg && threadIdx.x == 0) dbg[0] = globaltimer();
     int fail = 0;
     uint64_t deadline = 0;
     if (threadIdx.x == 0) {
@@ -793,6 +795,7 @@ __global__ void __launch_bounds__(kThreads) recv_batch_kernel(const __grid_const
       }
     }
     if (__syncthreads_or(fail)) return;
+    if (dbg && threadIdx.x == 0) dbg[1] = globaltimer();
     const uint8_t* zc_src = s_zc_src;
     // rotate the chunk ownership per message so the CTAs that carried the last chunks of
     // one message start the next one early
@@ -804,6 +807,7 @@ __global__ void __launch_bounds__(kThreads) recv_batch_kernel(const __grid_const
         const uint64_t len = min(a.chunk, a.bytes - off);
         if (zc_src) {
           cta_copy<true>(a.dst + off, zc_src + off, len);
+          if (dbg && threadIdx.x == 0 && c == first) dbg[2] = globaltimer();
           continue;
         }
         int f = 0;
@@ -817,6 +821,7 @@ __global__ void __launch_bounds__(kThreads) recv_batch_kernel(const __grid_const
     }
     __threadfence();
     __syncthreads();
+    if (dbg && threadIdx.x == 0) dbg[3] = globaltimer();
     if (threadIdx.x == 0) {
       if (atomicAdd(a.done, 1u) == gridDim.x - 1) {
         *a.done = 0;
