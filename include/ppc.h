@@ -338,7 +338,8 @@ ppc_status_t ppc_trace(ppc_comm_t* c, ppc_record_t* out, int* n);  /* synchroniz
 ppc_status_t ppc_kernel_times(ppc_comm_t* c, int kind, float* ms, int* n);
 /* Diagnostics (PPC_DBG_STAMPS=1 at ppc_create): per eager receive launch (the first 4096),
  * 128 CTA rows x 4 %globaltimer stamps — [0] released by griddepcontrol.wait, [1] header seen,
- * [2] first chunk moved (zero-copy pulls), [3] CTA done (0 = not reached / CTA absent) — and
+ * [2] first chunk moved (zero-copy pulls; SM id in bits 48-63, the timer's low 48 bits below),
+ * [3] CTA done (0 = not reached / CTA absent) — and
  * meta = (seq, dir, grid) per launch; synchronizes the device.  *n in: capacity in launches,
  * out: launches returned.  stamps has room for *n x 512 values, meta for *n x 3. */
 ppc_status_t ppc_debug_stamps(ppc_comm_t* c, unsigned long long* stamps, long long* meta, int* n);

@@ -767,7 +767,7 @@ ppc_status_t ppc_impl_recv_prepare(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t
     a.flags = h.i_flags;
     a.done = h.i_done;
   }
-  if (c->dbg && !c->capturing && c->dbg_meta.size() / 3 < (size_t)kDbgLaunches) {
+  if (c->dbg && c->dbg_meta.size() / 3 < (size_t)kDbgLaunches) {   // graph: last replay's
     a.dbg = c->dbg + (c->dbg_meta.size() / 3) * 4 * kDbgCtas;
     c->dbg_meta.push_back((long long)seq);
     c->dbg_meta.push_back(d);

@@ -184,6 +184,13 @@ __device__ __forceinline__ void latch(ErrWord* e, unsigned code, uint64_t seq, u
   __threadfence_system();
 }
 
+// PPC_DBG_STAMPS: %globaltimer (low 48 bits) with the SM id in the top 16 bits
+__device__ __forceinline__ uint64_t dbg_stamp_sm() {
+  uint32_t smid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  return ((uint64_t)smid << 48) | (globaltimer() & 0xFFFFFFFFFFFFull);
+}
+
 // Wait until *p >= target (wrap-safe); false on timeout.
 template <bool kSys = true>
 __device__ __forceinline__ bool wait_geq(const uint64_t* p, uint64_t target, uint64_t deadline) {
@@ -708,7 +715,7 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(const __grid_constant__ 
         skip = (uint64_t)kEarlyV * kThreads * sizeof(V32);
       }
       cta_copy<true>(a.dst + off + skip, zc_src + off + skip, len - skip);
-      if (dbg && threadIdx.x == 0 && c == it.first) dbg[2] = globaltimer();
+      if (dbg && threadIdx.x == 0 && c == it.first) dbg[2] = dbg_stamp_sm();
       continue;
     }
     int f = 0;
@@ -807,7 +814,7 @@ __global__ void __launch_bounds__(kThreads) recv_batch_kernel(const __grid_const
         const uint64_t len = min(a.chunk, a.bytes - off);
         if (zc_src) {
           cta_copy<true>(a.dst + off, zc_src + off, len);
-          if (dbg && threadIdx.x == 0 && c == first) dbg[2] = globaltimer();
+          if (dbg && threadIdx.x == 0 && c == first) dbg[2] = dbg_stamp_sm();
           continue;
         }
         int f = 0;

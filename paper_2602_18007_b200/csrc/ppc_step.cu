@@ -121,6 +121,19 @@ struct Stepper {
   // batched-receive grid (ppc_impl_recv_launch_batch), so the receiving CTAs flow from one
   // message to the next without a kernel boundary.  Their rendezvous commits and completion
   // bookkeeping follow the grid.
+  // Rendezvous commits of zero-copy sends from the caller's own buffers (x / g: never
+  // rewritten inside the step) are deferred to the step's end — one bounded credit wait per
+  // direction for the highest seq (credits are monotone and returned in order) instead of an
+  // event record on the compute stream + a wait kernel per message, so consecutive receive
+  // kernels on the compute stream stay PDL-chained.  Sends from the double-buffered step
+  // buffers keep their per-message commit (the buffer is reused two micro-batches later).
+  ZcSend last_commit[2];
+  bool has_last_commit[2] = {false, false};
+  void defer_commit(const ZcSend& z) {
+    last_commit[z.d] = z;
+    has_last_commit[z.d] = true;
+  }
+
   bool batching = false;
   std::vector<RecvArgs> pend;
   std::vector<std::pair<int, uint64_t>> pend_done;   // (dir, seq)
@@ -134,11 +147,7 @@ struct Stepper {
     }
     for (auto& dq : pend_done)
       if (ppc_status_t st = ppc_impl_recv_done(c, (ppc_dir_t)dq.first, dq.second, cs)) return st;
-    for (const ZcSend& z : pend_commit) {
-      if (ppc_status_t ts = time_mark(c, 0, cs, true)) return ts;
-      if (ppc_status_t ws = ppc_impl_zc_commit(c, z, cs, c->side[z.d])) return ws;
-      if (ppc_status_t ts = time_mark(c, 0, c->side[z.d], false)) return ts;
-    }
+    for (const ZcSend& z : pend_commit) defer_commit(z);
     pend.clear();
     pend_done.clear();
     pend_commit.clear();
@@ -332,9 +341,7 @@ struct Stepper {
             if (rs) return rs;
             if (!dst) sb.rpending[d][bi] = false;
             if (fuse) {   // the next op's send was published by this receive's kernel
-              if (ppc_status_t ts = time_mark(c, 0, cs, true)) return ts;
-              if (ppc_status_t ws = ppc_impl_zc_commit(c, z, cs, c->side[z.d])) return ws;
-              if (ppc_status_t ts = time_mark(c, 0, c->side[z.d], false)) return ts;
+              defer_commit(z);
               fused_next = true;
             }
           }
@@ -486,6 +493,19 @@ struct Stepper {
             }
             cudaStream_t s_pub = zc_cs ? cs : c->side[d];
             cudaStream_t s_done = zc_send ? (zc_cs ? c->side[d] : c->zcw[d]) : c->side[d];
+            if (zc_cs && send_buf == 0) {      // caller's buffer: publish now, commit at the end
+              ZcSend z;
+              if (ppc_status_t ps = ppc_impl_zc_prepare(c, (ppc_dir_t)d, send_src, bytes, m, &z))
+                return ps;
+              if (ppc_status_t ts = time_mark(c, 0, cs, true)) return ts;
+              CK(launch_publish(z.p, cs));
+              if (ppc_status_t ts = time_mark(c, 0, cs, false)) return ts;
+              defer_commit(z);
+              *progressed = true;
+              phase = 0;
+              ++i;
+              continue;
+            }
             ppc_status_t ss = ppc_impl_send_ex(c, (ppc_dir_t)d, send_src, bytes, m, s_pub, s_done);
             if (ss == PPC_ERR_WOULD_BLOCK) return PPC_OK;
             if (ss) return ss;
@@ -506,6 +526,11 @@ struct Stepper {
 
   ppc_status_t finish() {
     if (ppc_status_t fs = flush()) return fs;
+    for (int d = 0; d < 2; ++d)                  // the deferred rendezvous: one wait per dir
+      if (has_last_commit[d]) {
+        if (ppc_status_t ws = ppc_impl_zc_commit(c, last_commit[d], cs, c->side[d])) return ws;
+        has_last_commit[d] = false;
+      }
     if (used_ds) {                 // host outputs complete with the step
       CK(cudaEventRecord(c->sb.djoin, c->sb.ds));
       CK(cudaStreamWaitEvent(cs, c->sb.djoin, 0));

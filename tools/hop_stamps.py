@@ -22,6 +22,7 @@ import paper_2602_18007_b200 as ppc  # noqa: E402
 
 def main():
     assert os.environ.get("PPC_DBG_STAMPS") == "1", "run with PPC_DBG_STAMPS=1"
+    graph = "--graph" in sys.argv          # time CUDA-graph replays (the bench's mode)
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(rank)
     dist.init_process_group("gloo")
@@ -41,14 +42,25 @@ def main():
     args = ppc.StepArgs(M, n, n, x=X, g=G, y=out if rank == 1 else None, dx=out if rank == 0 else None)
     s = torch.cuda.Stream()
     times = []
+    g = None
+    if graph:                              # eager step first (buffers), then the capture
+        ppc.step_1f1b(comm, args, s)
+        torch.cuda.synchronize()
+        dist.barrier()
+        g = ppc.StepGraph([comm], [args], [s])
     for step in range(6):
         dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s)
-        ppc.step_1f1b(comm, args, s)
+        if g:
+            g.launch()
+        else:
+            ppc.step_1f1b(comm, args, s)
         e1.record(s)
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1) * 1e3)
+    if g:
+        g.destroy()
     st = comm.debug_stamps()
     allst = [None] * world
     dist.all_gather_object(allst, st)
@@ -59,8 +71,12 @@ def main():
                 rows = [x for x in rows if all(x)]
                 if not rows:
                     continue
+                for x in rows:                     # [2]: SM id << 48 | timer low 48 bits
+                    x.append(x[2] >> 48)
+                    x[2] = (x[1] & ~0xFFFFFFFFFFFF) | (x[2] & 0xFFFFFFFFFFFF)
                 col = lambda k: [x[k] for x in rows]
                 launches.append({"rank": r, "seq": seq, "dir": d, "ctas": len(rows),
+                                 "cta_sm_done": [(x[4], x[3] - min(col(1))) for x in rows],
                                  "rel_min": min(col(0)), "rel_max": max(col(0)),
                                  "seen_min": min(col(1)), "seen_max": max(col(1)),
                                  "first_min": min(col(2)) if all(col(2)) else None,
@@ -71,7 +87,8 @@ def main():
         hops = []
         for r, lst in per.items():
             lst.sort(key=lambda L: L["rel_min"])
-            last_steps = [L for L in lst if L["seq"] > 2 * M]      # the last steps only
+            # eager: the last steps; graph: the captured launches (the last replay's stamps)
+            last_steps = lst[-M:] if graph else [L for L in lst if L["seq"] > 2 * M]
             for prev, cur in zip(last_steps, last_steps[1:]):
                 hops.append({"rank": r, "seq": cur["seq"],
                              "boundary_us": (cur["rel_min"] - prev["done_max"]) * 1e-3,
@@ -81,7 +98,16 @@ def main():
                              "pull_us": (cur["done_max"] - cur["seen_min"]) * 1e-3,
                              "tail_us": (cur["done_max"] - cur["done_min"]) * 1e-3})
         med = lambda k: statistics.median(h[k] for h in hops)
-        summary = {"step_us": times[2:], "hops": len(hops),
+        # per SM: mean (done - first header seen) over the analysed launches
+        by_sm = {}
+        for r, lst in per.items():
+            for L in (lst[-M:] if graph else [L for L in lst if L["seq"] > 2 * M]):
+                for sm, t in L["cta_sm_done"]:
+                    by_sm.setdefault(sm, []).append(t * 1e-3)
+        sm_mean = sorted((statistics.mean(v), sm) for sm, v in by_sm.items())
+        summary = {"graph": graph, "step_us": times[2:], "hops": len(hops),
+                   "sm_done_us": {"fastest": sm_mean[:5], "slowest": sm_mean[-5:],
+                                  "n_sms": len(sm_mean)},
                    "median": {k: med(k) for k in ("boundary_us", "release_spread_us",
                                                   "rel_to_seen_us", "seen_spread_us",
                                                   "pull_us", "tail_us")}}
