@@ -201,7 +201,6 @@ cudaError_t preload_kernels();
 // PPC_PDL by ppc_create
 extern int g_pdl;
 extern int g_copy_tma_ctas;
-extern int g_copy_prefetch;    // PPC_COPY_PREFETCH
 extern int g_wait_value;       // PPC_WAIT_VALUE: eager credit waits as cuStreamWaitValue64
 extern std::atomic<unsigned long long> g_launches;   // ppc_launch_count
 // wait until *credit >= target (+ *seq_base when seq_base != nullptr: graph replay)

@@ -1039,15 +1039,6 @@ cudaError_t launch_add(void* dst, const void* src, size_t count, int dtype, cuda
 // last wave of chunks); otherwise per-CTA chunks of `chunk` bytes (cta_copy handles any
 // alignment).
 constexpr int kCopyU = 4;
-int g_copy_prefetch = 0;     // PPC_COPY_PREFETCH: copy_kernel loads with the L2::256B prefetch hint
-__device__ __forceinline__ V32 ld_src_pf(const V32* p) {
-  V32 r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(r.lo.x), "=r"(r.lo.y), "=r"(r.lo.z), "=r"(r.lo.w), "=r"(r.hi.x),
-                 "=r"(r.hi.y), "=r"(r.hi.z), "=r"(r.hi.w) : "l"(p));
-  return r;
-}
-template <bool kPf>
 __global__ void __launch_bounds__(kThreads, 2) copy_kernel(uint8_t* dst, const uint8_t* src,
                                                         uint64_t bytes, uint64_t chunk) {
   pdl_enter();
@@ -1068,7 +1059,7 @@ __global__ void __launch_bounds__(kThreads, 2) copy_kernel(uint8_t* dst, const u
     V32 v[kCopyU];
 #pragma unroll
     for (int j = 0; j < kCopyU; ++j)
-      if (b + j * stride < nv) v[j] = kPf ? ld_src_pf(s + b + j * stride) : ld_src(s + b + j * stride);
+      if (b + j * stride < nv) v[j] = ld_src(s + b + j * stride);
 #pragma unroll
     for (int j = 0; j < kCopyU; ++j)
       if (b + j * stride < nv) st_data(d + b + j * stride, v[j]);
@@ -1169,8 +1160,8 @@ cudaError_t launch_copy(void* dst, const void* src, uint64_t bytes, uint64_t chu
     return cudaLaunchKernelEx(&cfg, copy_tma_kernel, static_cast<uint8_t*>(dst),
                               static_cast<const uint8_t*>(src), bytes);
   }
-  return launch_k(g_copy_prefetch ? copy_kernel<true> : copy_kernel<false>, grid, kThreads, s,
-                  true, static_cast<uint8_t*>(dst), static_cast<const uint8_t*>(src), bytes, chunk);
+  return launch_k(copy_kernel, grid, kThreads, s, true, static_cast<uint8_t*>(dst),
+                  static_cast<const uint8_t*>(src), bytes, chunk);
 }
 
 // PPC_WAIT_VALUE=1 (opt-in, eager enqueues only): the credit wait becomes a stream memory
@@ -1263,8 +1254,7 @@ cudaError_t preload_kernels() {
       (const void*)wait_credit_kernel,     (const void*)set_seq_kernel,
       (const void*)add_kernel<float>,      (const void*)add_kernel<__half>,
       (const void*)add_kernel<__nv_bfloat16>, (const void*)add_kernel<int32_t>,
-      (const void*)copy_kernel<false>,     (const void*)copy_kernel<true>,
-      (const void*)xor_send_kernel,
+      (const void*)copy_kernel,            (const void*)xor_send_kernel,
       (const void*)splitmix_xor_kernel,
   };
   for (const void* f : fns) {
