@@ -48,6 +48,12 @@
  *   PPC_COPY_TMA_CTAS=0  virtual stages: >0 selects the TMA bulk hand-off copy with that
  *                        many CTAs (16-B aligned buffers); 0 = the SIMT copy kernel
  *                        (faster inside the overlapped step, profiles/r56_copy_engine_ab.jsonl)
+ *   PPC_STEP_BATCH=0     step driver (one process per GPU): the step's terminal receives (and
+ *                        their fused publications) as one batched-receive grid per step
+ *   PPC_PUB_FENCE=sys    fused publication flag release behind a system-scope fence; "gpu"
+ *                        uses a gpu-scope fence (−1 % N=2 step, outside the PTX model's
+ *                        guarantee for the peer — opt-in)
+ *   PPC_DBG_STAMPS=0     per-CTA receive-kernel stamps for ppc_debug_stamps (diagnostics)
  *   PPC_WAIT_VALUE=0     eager credit waits (zero-copy rendezvous, ppc_pp_wait_consumed) as
  *                        cuStreamWaitValue64 instead of the bounded 1-thread kernel: zero SMs,
  *                        but UNBOUNDED (no timeout) — measured opt-in, DESIGN.md §7
@@ -103,8 +109,10 @@ typedef struct {
   size_t max_msg_bytes;         /* ring slot payload capacity                                  */
   int ring_slots;               /* K; 0 => pp + 1 (1F1B occupancy bound + 1: sends never wait
                                    for a slot; SPEC's double buffering is K = 2)        */
-  int channels;                 /* MPDT analogue: SM engine = CTA groups, CE engine =
-                                   copy streams; 1..8; 0 => 1                                  */
+  int channels;                 /* MPDT analogue: a message's chunks split into this
+                                   many contiguous ranges, each moved by its own CTA group (SM
+                                   push, PULL staging and pulls, zero-copy pulls) or its own
+                                   copy-engine stream (CE engine); 1..8; 0 => 1               */
   size_t chunk_bytes;           /* flag granularity, multiple of 4096; 0 => 1 MiB              */
   ppc_engine_t engine;          /* data mover for sends                                        */
   int cta_per_channel;          /* SM engine CTAs per channel; 0 => auto                       */
