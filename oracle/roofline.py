@@ -3,8 +3,10 @@
 T* is O2 with zero stage compute and message time bytes / link bandwidth
 (900 GB/s per direction per GPU for NVLink 5, R4), in the "shared" link
 model (per-GPU egress/ingress shared max-min) and, as the optimistic bound, the
-"independent" model.  Parity unpinned vs hardware (it is a model); internally
-pinned through O2's tests (closed forms, SPEC examples).
+"independent" model.  Pinned (tests/test_oracle_schedule_events.py::test_o8_step_roofline_pins)
+by the hand-derived makespans: PP2 (M+1)*t and PP3 M3 8t shared / 6t independent.  As a
+model of the hardware it is only validated against measured steps (8-GPU projections,
+tests/test_projection_8gpu.py), not pinned.
 """
 from __future__ import annotations
 

@@ -257,3 +257,18 @@ def test_pp3_comm_only_makespan_hand_derived(mode, units):
     r = simulate(3, 3, 0.0, 0.0, nbytes, nbytes, LinkModel(bw=bw, mode=mode), K=4)
     validate_trace(r, 3)
     assert r.makespan == pytest.approx(units * nbytes / bw, rel=1e-12)
+
+
+def test_o8_step_roofline_pins():
+    """O8 (oracle/roofline.py): the comm-only T* equals the hand-derived makespans — PP2
+    (M+1)·t (R5) and PP3 M3 8t shared / 6t independent (§2a) — at 900 GB/s, and
+    tokens/s is M·seq / T (C2: 335.544 µs -> 97.66 M tok/s)."""
+    from oracle.roofline import step_roofline_us, tokens_per_s
+    nb = 32 << 20
+    t = nb / gbps_to_bytes_per_us(900)                       # 37.28 us
+    assert step_roofline_us(2, 8, nb) == pytest.approx(9 * t, rel=1e-12)
+    assert step_roofline_us(2, 8, nb) == pytest.approx(335.54432, abs=1e-5)
+    assert step_roofline_us(3, 3, nb, K=4) == pytest.approx(8 * t, rel=1e-12)
+    assert step_roofline_us(3, 3, nb, mode="independent", K=4) == pytest.approx(6 * t, rel=1e-12)
+    assert tokens_per_s(8, 4096, 335.54432) == pytest.approx(97.66e6, rel=1e-3)
+    assert tokens_per_s(8, 4096, 500.0, pipelines=2) == pytest.approx(2 * 8 * 4096 / 500e-6)
