@@ -115,6 +115,9 @@ def config_dict(wl, world):
             "hidden": wl["hidden"], "msg_bytes": wl["msg_bytes"], "engine": wl["engine"],
             "chunk_bytes": wl["chunk"], "channels": wl["channels"], "ring_slots": wl["slots"],
             "zero_copy_sends": wl["zc"], "cuda_graph": wl["graph"],
+            # N=1 hands boundaries over in HBM (two virtual stages), N>=2 over NVLink: the
+            # weak-scaling series is N = 2, 4, 8 (same per-pipeline work on the same link)
+            "transport": "hbm (intra-device)" if wl["virtual"] else "nvlink (peer pulls)",
             "l2": (f"inputs larger than L2 (M x {wl['msg_bytes'] / 2**20:g} MiB per stage per "
                    f"direction = {per_dir / 2**20:g} MiB > 126 MB)" if per_dir > 126e6 else
                    "inputs fit in L2: latency run, not a bench line")}

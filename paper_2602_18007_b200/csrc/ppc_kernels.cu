@@ -873,7 +873,12 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(GatherArgs a) {
   const uint32_t units = a.tp * a.n_chunks;
   for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
     const uint32_t t = (u + a.my_tp) % a.tp, c = u / a.tp;
-    if (!s_src[t]) {
+    // every thread reads s_src[t] before thread 0 may set it below: a warp still finishing
+    // the previous unit's copy must not see it already set and skip the barrier the others
+    // wait at (cta_copy has no barrier, so warps drift apart by a loaded NVLink round trip)
+    const bool need = !s_src[t];
+    __syncthreads();
+    if (need) {
       int fail = 0;
       if (threadIdx.x == 0) {
         if (!wait_geq<true>(a.hdr_flag[t], a.seq, deadline)) {
