@@ -35,6 +35,12 @@
  *                        first 64 KiB of each CTA's first chunk into registers meanwhile
  *   PPC_FUSE_PUBLISH=1   step driver: a zero-copy source op's publication rides on the
  *                        preceding terminal receive kernel
+ *   PPC_PUB_BLOCK0=1     that fused publication's flag is released by the receive's block 0
+ *                        (header already fenced at system scope) once every worker CTA has
+ *                        arrived, instead of by the last worker behind a second system fence
+ *   PPC_RECV_CHAIN=1     step driver: a receive enqueued right behind another receive starts
+ *                        on that receive's posted end of data phase (a local device word)
+ *                        instead of at griddepcontrol.wait (its grid exit + PDL release)
  *   PPC_ZC_SIDE=0        step driver: publish zero-copy sends on the send stream instead
  *                        of the compute stream
  *   PPC_ZC_STEPBUFS=1    the step driver's buffers (in the arena) are zero-copy sources

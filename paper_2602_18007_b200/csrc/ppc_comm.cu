@@ -161,6 +161,8 @@ ppc_status_t ppc_create(const ppc_config_t* cfg, int world, int rank, int cuda_d
   if (c->cfg.channels == 0) c->cfg.channels = 1;
   c->zc_side = env_int("PPC_ZC_SIDE", 0) != 0;
   c->fuse_publish = env_int("PPC_FUSE_PUBLISH", 1) != 0;
+  c->recv_chain = env_int("PPC_RECV_CHAIN", 1) != 0;
+  c->pub_b0 = env_int("PPC_PUB_BLOCK0", 1) != 0;
   c->zc_stepbufs = env_int("PPC_ZC_STEPBUFS", 1) != 0;
   c->step_inplace = env_int("PPC_STEP_INPLACE", 0) != 0;
   ppc::g_pdl = env_int("PPC_PDL", 1) != 0 ? 1 : 0;
@@ -212,6 +214,9 @@ ppc_status_t ppc_create(const ppc_config_t* cfg, int world, int rank, int cuda_d
           cudaMemcpy(c->err_dev, &w, sizeof(w), cudaMemcpyHostToDevice) != cudaSuccess)
         return fail(PPC_ERR_CUDA);
     }
+    if (cudaMalloc(&c->rchain, 2 * sizeof(uint64_t)) != cudaSuccess ||
+        cudaMemset(c->rchain, 0, 2 * sizeof(uint64_t)) != cudaSuccess)
+      return fail(PPC_ERR_CUDA);
     if (cudaIpcGetMemHandle(&b.ipc, c->arena) != cudaSuccess) return fail(PPC_ERR_CUDA);
     if (cudaDeviceGetPCIBusId(b.busid, sizeof(b.busid), cuda_device) != cudaSuccess)
       return fail(PPC_ERR_CUDA);
@@ -711,7 +716,7 @@ ppc_status_t ppc_pp_recv(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t bytes, lo
 // Virtual stages: the stream waits for the matching send's event first.
 ppc_status_t ppc_impl_recv_prepare(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t bytes,
                                    long long mb, cudaStream_t s, const PublishArgs* pub,
-                                   RecvArgs* out) {
+                                   RecvArgs* out, const RecvChainRef* prev) {
   ppc_status_t st = check_live(c);
   if (st) return st;
   if (d != PPC_FWD && d != PPC_BWD) return PPC_ERR_INVALID_ARG;
@@ -755,7 +760,23 @@ ppc_status_t ppc_impl_recv_prepare(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t
   a.channels = c->cfg.engine == PPC_ENGINE_CE ? 1u : (uint32_t)std::max(1, c->cfg.channels);
   if (pub) {
     a.has_pub = 1;
+    a.pub_b0 = c->pub_b0 ? 1u : 0u;
     a.pub = *pub;
+  }
+  if (c->recv_chain && !c->local_mode) {
+    a.chain_post = c->rchain + d;
+    if (prev && c->cfg.engine != PPC_ENGINE_CE) {
+      a.chain_wait = c->rchain + prev->dir;
+      a.chain_seq = prev->seq;
+      if (c->capturing) {         // the predecessor's seq relative to its graph base
+        if (prev->seq <= c->cap_recv[prev->dir]) {
+          a.chain_wait = nullptr;   // captured before this graph: plain PDL wait
+        } else {
+          a.chain_base = c->dseq + 2 + prev->dir;
+          a.chain_seq = prev->seq - c->cap_recv[prev->dir];
+        }
+      }
+    }
   }
   if (c->capturing) {             // graph: relative seq, slot resolved on device
     a.sr = {c->dseq + 2 + d, (uint64_t)c->lay.stride, (uint32_t)c->K,
@@ -784,11 +805,12 @@ ppc_status_t ppc_impl_recv_done(ppc_comm_t* c, ppc_dir_t d, uint64_t seq, cudaSt
 }
 
 ppc_status_t ppc_impl_recv_ex(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t bytes,
-                              long long mb, cudaStream_t s, const PublishArgs* pub) {
+                              long long mb, cudaStream_t s, const PublishArgs* pub,
+                              const RecvChainRef* prev) {
   if (!c) return PPC_ERR_STATE;
   DeviceGuard g(c->device);
   RecvArgs a;
-  ppc_status_t st = ppc_impl_recv_prepare(c, d, buf, bytes, mb, s, pub, &a);
+  ppc_status_t st = ppc_impl_recv_prepare(c, d, buf, bytes, mb, s, pub, &a, prev);
   if (st) return st;
   if (ppc_status_t ts = time_mark(c, 1, s, true)) return ts;
   CK(launch_recv(a, recv_grid(c, a.n_chunks), c->sys_scope, s));
@@ -1196,6 +1218,7 @@ ppc_status_t ppc_destroy(ppc_comm_t* c) {
     if (c->arena) cudaFree(c->arena);
     if (c->err_host) cudaFreeHost(c->err_host);
     if (c->err_dev) cudaFree(c->err_dev);
+    if (c->rchain) cudaFree(c->rchain);
   }
   delete c;
   return PPC_OK;

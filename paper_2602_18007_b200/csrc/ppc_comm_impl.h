@@ -148,6 +148,11 @@ struct ppc_comm {
   uint8_t* arena = nullptr;
   ErrHost* err_host = nullptr;     // mapped host record (polled by the host)
   ErrWord* err_dev = nullptr;      // device claim word + the record's device pointer
+  // chained receives: per direction, the highest seq whose receive finished its data phase
+  // (device memory, monotone); chain_* = the receive last enqueued by the step driver
+  uint64_t* rchain = nullptr;
+  bool recv_chain = true;          // PPC_RECV_CHAIN (default on)
+  bool pub_b0 = true;              // PPC_PUB_BLOCK0: block 0 releases a fused publication
   bool connected = false, poisoned = false, local_mode = false;
   bool sys_scope = true;   // a PP neighbour is another GPU: .sys fences, NVLink-sized grids
   int spin_cap = 64;       // max CTAs of a spinning grid (8 when a peer shares our GPU in
@@ -219,14 +224,22 @@ ppc_status_t ppc_impl_zc_prepare(ppc_comm_t* c, ppc_dir_t d, const void* buf, si
 // rendezvous wait of a published zero-copy send on s_wait (after the work queued on s)
 ppc_status_t ppc_impl_zc_commit(ppc_comm_t* c, const ZcSend& z, cudaStream_t s,
                                 cudaStream_t s_wait);
-// ppc_pp_recv whose kernel also publishes `pub` after completing (nullptr: plain receive)
+// The receive a chained receive starts behind (its direction and absolute seq).
+struct RecvChainRef {
+  int dir;
+  uint64_t seq;
+};
+// ppc_pp_recv whose kernel also publishes `pub` after completing (nullptr: plain receive).
+// prev != nullptr: the caller guarantees that the last thing it enqueued on s is that
+// receive's kernel (nothing in between), so this one may start on its posted completion.
 ppc_status_t ppc_impl_recv_ex(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t bytes,
-                              long long mb, cudaStream_t s, const PublishArgs* pub);
+                              long long mb, cudaStream_t s, const PublishArgs* pub,
+                              const RecvChainRef* prev = nullptr);
 // the same split in three: arguments + bookkeeping, one grid for n prepared receives, and
 // the per-message completion bookkeeping (virtual stages: the recvd event)
 ppc_status_t ppc_impl_recv_prepare(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t bytes,
                                    long long mb, cudaStream_t s, const PublishArgs* pub,
-                                   RecvArgs* out);
+                                   RecvArgs* out, const RecvChainRef* prev = nullptr);
 ppc_status_t ppc_impl_recv_launch_batch(ppc_comm_t* c, const RecvArgs* as, int n,
                                         cudaStream_t s);
 ppc_status_t ppc_impl_recv_done(ppc_comm_t* c, ppc_dir_t d, uint64_t seq, cudaStream_t s);

@@ -123,7 +123,16 @@ struct RecvArgs {
   // fused publication (step driver): when has_pub, the last CTA publishes `pub` (the next
   // op's zero-copy send) right after releasing this receive's credit
   uint32_t has_pub;
+  uint32_t pub_b0;              // the publication is released by block 0 (PPC_PUB_BLOCK0)
   PublishArgs pub;
+  // chained receives (step driver, PPC_RECV_CHAIN): a receive whose stream predecessor is
+  // another receive starts when that one has finished its data phase — posted as its
+  // resolved seq in a local per-direction word — instead of at griddepcontrol.wait, i.e.
+  // after the predecessor grid's exit and PDL release (and off its publication fence)
+  uint64_t* chain_post;         // this receive's direction word (atomicMax of its seq), or nullptr
+  const uint64_t* chain_wait;   // the predecessor's direction word, or nullptr (plain PDL wait)
+  const uint64_t* chain_base;   // graph capture: the predecessor's sequence base, else nullptr
+  uint64_t chain_seq;           // the predecessor's seq (relative to *chain_base when set)
 };
 extern int g_recv_early;
 cudaError_t launch_publish(const PublishArgs& a, cudaStream_t s);

@@ -564,7 +564,7 @@ __device__ __forceinline__ bool fused_publish_header(const PublishArgs* p0) {
 // critical path), then this receive's credit.  A second release would wait for the first
 // store's NVLink acknowledgement.
 __device__ __forceinline__ void fused_publish_flag(const PublishArgs* p0, uint64_t* credit,
-                                                  uint64_t seq) {
+                                                  uint64_t seq, bool fenced = false) {
   uint64_t pseq = p0->seq;
   uint64_t* flag = p0->hdr_flag;
   if (p0->sr.base) {                  // graph replay: resolve seq and slot (as resolve())
@@ -577,8 +577,12 @@ __device__ __forceinline__ void fused_publish_flag(const PublishArgs* p0, uint64
   // returned before its arrival, and this CTA saw all arrivals — so only gpu-scope ordering
   // is left to establish here.  Opt-in A/B; the default keeps the full
   // system-scope release.
-  if (p0->gpu_fence) asm volatile("fence.acq_rel.gpu;" ::: "memory");
-  else fence_acq_rel_sys();
+  // fenced: the caller is block 0, whose own system fence after the header stores
+  // (fused_publish_header) already orders them before these stores
+  if (!fenced) {
+    if (p0->gpu_fence) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    else fence_acq_rel_sys();
+  }
   st_relaxed_sys(flag, pseq);
   st_relaxed_sys(credit, seq);
   if (ppc_record_t* r = p0->rec) {
@@ -589,14 +593,50 @@ __device__ __forceinline__ void fused_publish_flag(const PublishArgs* p0, uint64
 }
 
 // kPub: the variant with the fused publication (step driver, terminal receives of a
-// comm-only PP2 step); it needs 88 registers (one CTA per SM), so the plain variant, which
-// shares SMs with the push kernels of deeper pipelines, is kept at 64.
+// comm-only PP2 step).  Both variants need ~90 registers: one 512-thread CTA per SM.
 // mapped base of a zero-copy source segment on this GPU; 0 if never imported
 __device__ __forceinline__ uint64_t zc_base(const RecvArgs& a, uint32_t seg) {
   return seg == kArenaSeg ? (uint64_t)(uintptr_t)a.peer_arena
        : (a.seg_tab && seg < (uint32_t)kMaxSeg) ? a.seg_tab[seg] : 0;
 }
 constexpr int kEarlyV = 4;                    // V32 vectors per thread pulled early (64 KiB/CTA)
+
+// Chained receive entry (RecvArgs::chain_wait): instead of griddepcontrol.wait (which
+// returns only after the predecessor grid has exited — its last CTA's publication fence
+// included — and PDL has released us), thread 0 waits (bounded) until the predecessor
+// receive has posted the end of its data phase; only then may the NEXT kernel get resident,
+// so at most two receive grids are resident at a time, as with plain PDL.  The
+// predecessor's sequence base (graph replay) was written by set_seq_kernel, which
+// completed before the predecessor passed its own griddepcontrol.wait and therefore before
+// we could be launched.  false: timed out (error latched).
+__device__ __forceinline__ bool chain_enter(const RecvArgs& a0) {
+  int fail = 0;
+  if (threadIdx.x == 0) {
+    const uint64_t target = a0.chain_seq + (a0.chain_base ? *a0.chain_base : 0);
+    if (!wait_geq<false>(a0.chain_wait, target, globaltimer() + a0.timeout_ns)) {
+      latch(a0.err, PPC_ERR_TIMEOUT, a0.seq, 0x700u);
+      fail = 1;
+    }
+  }
+  fail = __syncthreads_or(fail);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  return !fail;
+}
+// block 0 of a kPub receive: wait (bounded) until the n worker CTAs have arrived
+__device__ __forceinline__ bool wait_arrivals(const uint32_t* done, uint32_t n, uint64_t deadline) {
+  int spins = 0;
+  for (;;) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(done) : "memory");
+    if (v >= n) return true;
+    if (((++spins) & 255) == 0 && globaltimer() > deadline) return false;
+  }
+}
+// end of a receive's data phase (its last CTA, after the done count): post its seq
+__device__ __forceinline__ void chain_post(const RecvArgs& a) {
+  if (a.chain_post)
+    atomicMax(reinterpret_cast<unsigned long long*>(a.chain_post), (unsigned long long)a.seq);
+}
 
 template <bool kSys, bool kPub, bool kEarly = false>
 __global__ void __launch_bounds__(kThreads) recv_kernel(const __grid_constant__ RecvArgs a0) {
@@ -640,9 +680,13 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(const __grid_constant__ 
       pre_ok = true;
     }
   }
-  pdl_enter();
-  // PPC_DBG_STAMPS (diagnostics): per CTA [0] released by griddepcontrol.wait, [1] header
-  // seen, [2] first chunk moved, [3] done
+  if (!kEarly && a0.chain_wait) {
+    if (!chain_enter(a0)) return;
+  } else {
+    pdl_enter();
+  }
+  // PPC_DBG_STAMPS (diagnostics): per CTA [0] released by griddepcontrol.wait (or the
+  // chain), [1] header seen, [2] first chunk moved, [3] done
   uint64_t* const dbg = a0.dbg ? a0.dbg + 4 * blockIdx.x : nullptr;
   if (dbg && threadIdx.x == 0) dbg[0] = globaltimer();
   const RecvArgs a = resolve(a0);
@@ -729,10 +773,29 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(const __grid_constant__ 
   __threadfence();                 // slot reads + user-buffer writes before the credit
   __syncthreads();
   if (dbg && threadIdx.x == 0) dbg[3] = globaltimer();
-  if (threadIdx.x == 0) {
+  if (kPub && !kEarly && a0.pub_b0 && threadIdx.x == 0) {
+    // The publication is released by block 0, not by the last worker: block 0 fenced its
+    // header stores at system scope when it wrote them (off the critical path), so once every
+    // worker has arrived it stores the flag and the credit without a second system fence —
+    // a fence.sys in the last worker (which has just stored its share of the message) is
+    // ~1.3 us on the 1F1B critical path.  Workers' pulls are complete (loads returned) at
+    // arrival; the published payload was written by earlier kernels.
+    if (blockIdx.x != 0) {
+      atomicAdd(a.done, 1u);
+    } else if (!wait_arrivals(a.done, gridDim.x - 1, deadline)) {
+      latch(a.err, PPC_ERR_TIMEOUT, a.seq, 0x800u);
+    } else {
+      *a.done = 0;                 // next use of this slot is stream-ordered after us
+      __threadfence();
+      chain_post(a);
+      fused_publish_flag(&a0.pub, a.peer_credit, a.seq, true);
+      if (a.rec) a.rec->t_end_ns = (long long)globaltimer();
+    }
+  } else if (threadIdx.x == 0) {
     if (atomicAdd(a.done, 1u) == gridDim.x - 1) {
       *a.done = 0;                 // next use of this slot is stream-ordered after us
       __threadfence();
+      chain_post(a);               // a chained successor may start now (before our fence)
       if (kPub) {
         fused_publish_flag(&a0.pub, a.peer_credit, a.seq);
       } else {
@@ -833,6 +896,7 @@ __global__ void __launch_bounds__(kThreads) recv_batch_kernel(const __grid_const
       if (atomicAdd(a.done, 1u) == gridDim.x - 1) {
         *a.done = 0;
         __threadfence();
+        chain_post(a);
         if (kPub && a.has_pub) {
           fused_publish_flag(&b.a[i].pub, a.peer_credit, a.seq);
         } else {

@@ -134,6 +134,14 @@ struct Stepper {
     has_last_commit[z.d] = true;
   }
 
+  // Chained receives (PPC_RECV_CHAIN): a terminal receive into a device destination whose
+  // kernel also carries the next op's publication enqueues nothing else on the compute
+  // stream, and neither does that next (fused source) op; so when the op after it is a
+  // receive again, the last thing on the stream is the previous receive's kernel, and the
+  // new receive may start on that kernel's posted completion (ppc_impl_recv_ex prev).
+  RecvChainRef chain_prev{0, 0};
+  size_t chain_op = (size_t)-1;   // op index of that receive; chained iff i == chain_op + 2
+
   bool batching = false;
   std::vector<RecvArgs> pend;
   std::vector<std::pair<int, uint64_t>> pend_done;   // (dir, seq)
@@ -335,14 +343,19 @@ struct Stepper {
               if (ppc_status_t w = before_write(1, d, bi, cs)) return w;
             ZcSend z;
             const bool fuse = dst && fusable_next(&z);
+            const bool chained = chain_op != (size_t)-1 && i == chain_op + 2;
             ppc_status_t rs = ppc_impl_recv_ex(c, (ppc_dir_t)d, r, bytes, m, cs,
-                                               fuse ? &z.p : nullptr);
+                                               fuse ? &z.p : nullptr,
+                                               chained ? &chain_prev : nullptr);
             if (rs == PPC_ERR_WOULD_BLOCK) return PPC_OK;
             if (rs) return rs;
             if (!dst) sb.rpending[d][bi] = false;
+            chain_op = (size_t)-1;
             if (fuse) {   // the next op's send was published by this receive's kernel
               defer_commit(z);
               fused_next = true;
+              chain_prev = {d, c->ch[d].recv_seq};   // dst: terminal, nothing follows on cs
+              chain_op = i;
             }
           }
           direct = dst != nullptr;
