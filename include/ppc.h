@@ -38,6 +38,9 @@
  *   PPC_PUB_BLOCK0=1     that fused publication's flag is released by the receive's block 0
  *                        (header already fenced at system scope) once every worker CTA has
  *                        arrived, instead of by the last worker behind a second system fence
+ *   PPC_PULL_DYN=1       zero-copy pulls: every warp claims 4 KiB units of the message from
+ *                        a per-slot counter (CTAs with faster NVLink paths take more) instead
+ *                        of static chunk ranges per CTA (cfg.channels does not apply then)
  *   PPC_RECV_CHAIN=1     step driver: a receive enqueued right behind another receive starts
  *                        on that receive's posted end of data phase (a local device word)
  *                        instead of at griddepcontrol.wait (its grid exit + PDL release)

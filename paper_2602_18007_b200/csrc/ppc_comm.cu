@@ -163,6 +163,7 @@ ppc_status_t ppc_create(const ppc_config_t* cfg, int world, int rank, int cuda_d
   c->fuse_publish = env_int("PPC_FUSE_PUBLISH", 1) != 0;
   c->recv_chain = env_int("PPC_RECV_CHAIN", 1) != 0;
   c->pub_b0 = env_int("PPC_PUB_BLOCK0", 1) != 0;
+  c->pull_dyn = env_int("PPC_PULL_DYN", 1) != 0;
   c->zc_stepbufs = env_int("PPC_ZC_STEPBUFS", 1) != 0;
   c->step_inplace = env_int("PPC_STEP_INPLACE", 0) != 0;
   ppc::g_pdl = env_int("PPC_PDL", 1) != 0 ? 1 : 0;
@@ -744,6 +745,8 @@ ppc_status_t ppc_impl_recv_prepare(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t
   a.flags = h.i_flags + (size_t)slot * std::max<uint32_t>(c->lay.max_chunks, 1);
   a.peer_credit = h.peer_credit;
   a.done = h.i_done + slot;
+  a.next = h.i_done + c->K + slot;
+  a.dyn = c->pull_dyn ? 1u : 0u;
   a.bytes = bytes;
   a.chunk = c->chunk;
   a.n_chunks = n_chunks;
@@ -787,6 +790,7 @@ ppc_status_t ppc_impl_recv_prepare(ppc_comm_t* c, ppc_dir_t d, void* buf, size_t
     a.hdr_flag = h.i_hdr_flag;
     a.flags = h.i_flags;
     a.done = h.i_done;
+    a.next = h.i_done + c->K;
   }
   if (c->dbg && c->dbg_meta.size() / 3 < (size_t)kDbgLaunches) {   // graph: last replay's
     a.dbg = c->dbg + (c->dbg_meta.size() / 3) * 4 * kDbgCtas;

@@ -66,7 +66,8 @@ struct Layout {
       off = round_up(off + (size_t)K * std::max<uint32_t>(max_chunks, 1) * 8, 256);
     }
     for (int d = 0; d < 2; ++d) { credit[d] = off; off += 256; }
-    for (int d = 0; d < 2; ++d) { done[d] = off; off = round_up(off + (size_t)K * 4, 256); }
+    // per slot: the receive's arrival counter, then (K further) its pull-unit claim counter
+    for (int d = 0; d < 2; ++d) { done[d] = off; off = round_up(off + (size_t)K * 8, 256); }
     for (int d = 0; d < 2; ++d) { push_done[d] = off; off += 256; }
     // TP-sliced receives: receivers of one stage count finished pulls here (monotone)
     for (int d = 0; d < 2; ++d) { gdone[d] = off; off += 256; }
@@ -153,6 +154,7 @@ struct ppc_comm {
   uint64_t* rchain = nullptr;
   bool recv_chain = true;          // PPC_RECV_CHAIN (default on)
   bool pub_b0 = true;              // PPC_PUB_BLOCK0: block 0 releases a fused publication
+  bool pull_dyn = true;            // PPC_PULL_DYN: zero-copy pulls claim 4 KiB units per warp
   bool connected = false, poisoned = false, local_mode = false;
   bool sys_scope = true;   // a PP neighbour is another GPU: .sys fences, NVLink-sized grids
   int spin_cap = 64;       // max CTAs of a spinning grid (8 when a peer shares our GPU in

@@ -108,6 +108,8 @@ struct RecvArgs {
   const uint64_t* flags;
   uint64_t* peer_credit;        // sender's credit word (peer memory)
   uint32_t* done;               // local completion counter of this slot
+  uint32_t* next;               // zero-copy pull: unit claim counter of this slot (dyn)
+  uint32_t dyn;                 // zero-copy pull: warps claim 4 KiB units (PPC_PULL_DYN)
   uint64_t bytes, chunk;
   uint32_t n_chunks;
   uint64_t seq;

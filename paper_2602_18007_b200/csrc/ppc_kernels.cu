@@ -316,6 +316,7 @@ __device__ __forceinline__ RecvArgs resolve(RecvArgs a) {
     a.hdr_flag += slot;
     a.flags += slot * a.sr.fstride;
     a.done += slot;
+    a.next += slot;
   }
   return a;
 }
@@ -600,6 +601,7 @@ __device__ __forceinline__ uint64_t zc_base(const RecvArgs& a, uint32_t seg) {
        : (a.seg_tab && seg < (uint32_t)kMaxSeg) ? a.seg_tab[seg] : 0;
 }
 constexpr int kEarlyV = 4;                    // V32 vectors per thread pulled early (64 KiB/CTA)
+constexpr uint32_t kPullUnit = 4096;          // PPC_PULL_DYN: bytes per warp claim (4 V32 / lane)
 
 // Chained receive entry (RecvArgs::chain_wait): instead of griddepcontrol.wait (which
 // returns only after the predecessor grid has exited — its last CTA's publication fence
@@ -745,8 +747,29 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(const __grid_constant__ 
   // stores, system fence); it carries no chunks, else it would be the tail CTA whose
   // completion gates the publication (launch_recv adds one CTA for it)
   const uint32_t w0 = (kPub && !kEarly) ? 1u : 0u;
-  const ChanIter it = blockIdx.x >= w0 ? chan_iter(a.n_chunks, a.channels, blockIdx.x - w0,
-                                                   gridDim.x - w0) : ChanIter{0, 0, 1};
+  if (!kEarly && zc_src && a.dyn) {
+    // PPC_PULL_DYN: every warp of the worker CTAs claims 4 KiB units of the message from the
+    // slot's counter (claim of the next unit in flight with the current unit's loads), so
+    // CTAs on SMs with faster NVLink paths take more units and all finish together —
+    // with static chunk ranges the first and last CTA finish ~7 us apart
+    if (blockIdx.x >= w0) {
+      const uint32_t lane = threadIdx.x & 31;
+      const uint64_t n_units = (a.bytes + kPullUnit - 1) / kPullUnit;
+      uint32_t u = lane == 0 ? atomicAdd(a.next, 1u) : 0u;
+      u = __shfl_sync(0xffffffffu, u, 0);
+      bool first = true;
+      while (u < n_units) {
+        const uint32_t nx = lane == 0 ? atomicAdd(a.next, 1u) : 0u;
+        const uint64_t off = (uint64_t)u * kPullUnit;
+        cta_copy<true>(a.dst + off, zc_src + off, min((uint64_t)kPullUnit, a.bytes - off), lane, 32);
+        if (dbg && threadIdx.x == 0 && first) dbg[2] = dbg_stamp_sm();
+        first = false;
+        u = __shfl_sync(0xffffffffu, nx, 0);
+      }
+    }
+  }
+  const ChanIter it = (blockIdx.x >= w0 && !(!kEarly && zc_src && a.dyn))
+      ? chan_iter(a.n_chunks, a.channels, blockIdx.x - w0, gridDim.x - w0) : ChanIter{0, 0, 1};
   for (uint32_t c = it.first; c < it.end; c += it.step) {
     const uint64_t off = (uint64_t)c * a.chunk;
     const uint64_t len = min(a.chunk, a.bytes - off);
@@ -786,6 +809,7 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(const __grid_constant__ 
       latch(a.err, PPC_ERR_TIMEOUT, a.seq, 0x800u);
     } else {
       *a.done = 0;                 // next use of this slot is stream-ordered after us
+      *a.next = 0;                 // every claim (one past the end per warp) is in
       __threadfence();
       chain_post(a);
       fused_publish_flag(&a0.pub, a.peer_credit, a.seq, true);
@@ -794,6 +818,7 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(const __grid_constant__ 
   } else if (threadIdx.x == 0) {
     if (atomicAdd(a.done, 1u) == gridDim.x - 1) {
       *a.done = 0;                 // next use of this slot is stream-ordered after us
+      *a.next = 0;
       __threadfence();
       chain_post(a);               // a chained successor may start now (before our fence)
       if (kPub) {
