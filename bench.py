@@ -809,6 +809,17 @@ def main():
                      "traffic": ncu_traffic("recv_n2"),
                      "traffic_counters": "ncu nvlrx__bytes_data_user.sum + nvltx__bytes_data_user"
                                          ".sum per launch (profiles/ncu_traffic.json)"})
+        nvl = ncu_traffic("recv_n2_nvl_totals")
+        if nvl:
+            # what an SM pull can reach on these links: every 128-B read costs 16 B of response
+            # header (rx) and a 24-B request travelling the other way (tx), so with both
+            # directions pulling each link direction carries rx + the reverse pull's tx
+            bi = roof["peak"] * nvl["user_bytes"] / (nvl["nvlrx_bytes"] + nvl["nvltx_bytes"])
+            uni = roof["peak"] * nvl["user_bytes"] / nvl["nvlrx_bytes"]
+            roof["protocol_bound"] = {
+                "bidir_gbps": bi, "uni_gbps": uni, "frac_bidir": roof["achieved"] / bi,
+                "how": "900 GB/s x user / NVLink bytes (incl. protocol) of one pull, from the "
+                       "committed ncu NVLink counters (profiles/ncu_traffic.json)"}
     elif roof is not None:
         roof.update({"kernel": "ppc::push_ws_kernel (SM push over NVLink)",
                      "achieved": roof["event_achieved"], "avg_launch_us": roof["event_launch_us"],

@@ -8,6 +8,7 @@
 #   n4b   (4 GPUs) exposure by mover (zero-copy / push / produce-in-place), gather
 #   n4c   (4 GPUs) 8-rank bench rehearsal, gather, 4-rank multi tests
 #   partition  (2 GPUs) NEXT-3 planner vs measured for 16-16 / 15-17 / 14-18
+#   final2  (2 GPUs) final build: N=2 line, 500-step stability, NVLink counters, C5 sweep
 # Logs: gpurun_out/TAG_*.  Copies of the judged ones are in profiles/round2/.
 PASS=$1; T=${2:-$1}
 mkdir -p gpurun_out
@@ -107,8 +108,21 @@ pass_partition() {
   done
 }
 
+# final (2 GPUs): the N=2 line, 500-step stability, NVLink counters of the zero-copy pull, C5
+pass_final2() {
+  trun 2 bench.py --gpus 2 > gpurun_out/${T}_bench2.log 2>&1; grep '^{"metric' gpurun_out/${T}_bench2.log | cut -c1-300
+  trun 2 bench_stability.py --steps 500 --out gpurun_out/${T}_stability_n2.json > gpurun_out/${T}_stability.log 2>&1
+  tail -n 1 gpurun_out/${T}_stability.log | cut -c1-300
+  timeout 600 ncu --metrics gpu__time_duration.sum,nvlrx__bytes_data_user.sum,nvltx__bytes_data_user.sum,nvlrx__bytes.sum,nvltx__bytes.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+    -k regex:"recv_kernel" --csv python tools/ncu_xdev.py --mode zc > gpurun_out/${T}_ncu_xdev_zc.csv 2>&1
+  tail -n 4 gpurun_out/${T}_ncu_xdev_zc.csv
+  trun 2 bench_sweep.py --sizes 64K,1M,16M,32M,64M,128M,256M,1G --sm 64:512K --ce 1 --zc 64:256K:a,64:256K:ab \
+    --modes uni,bidir --comparators ce_copy --out gpurun_out/${T}_sweep.jsonl > gpurun_out/${T}_sweep.log 2>&1
+  tail -n 2 gpurun_out/${T}_sweep.log
+}
+
 case $PASS in
-  n2|n2b|n2c|n4|n4b|n4c|partition) pass_$PASS ;;
-  *) echo "usage: tools/perf.sh n2|n2b|n2c|n4|n4b|n4c|partition [TAG]"; exit 2 ;;
+  n2|n2b|n2c|n4|n4b|n4c|partition|final2) pass_$PASS ;;
+  *) echo "usage: tools/perf.sh n2|n2b|n2c|n4|n4b|n4c|partition|final2 [TAG]"; exit 2 ;;
 esac
 true
