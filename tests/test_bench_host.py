@@ -107,3 +107,15 @@ def test_gloo_bootstrap_world(world):
         pp_m, pp_b = groups[ppc.GROUP_PP]
         assert tp_m == next(x for x in g["tp"] if rank in x) and tp_b == ppc.BACKEND_NCCL
         assert pp_m == next(x for x in g["pp"] if rank in x) and pp_b == ppc.BACKEND_PEER
+
+
+def test_committed_ncu_counters_give_the_pull_protocol_bounds():
+    """The NVLink counters behind roofline.protocol_bound (profiles/ncu_traffic.json): user
+    bytes = one 32 MiB message; 16 B of response header per 128 B on rx, 24 B of request per
+    128 B on tx — so 800 GB/s one way, 685.7 GB/s with both directions pulling."""
+    nvl = bench.ncu_traffic("recv_n2_nvl_totals")
+    assert nvl["user_bytes"] == 32 << 20
+    assert nvl["nvlrx_bytes"] - nvl["user_bytes"] == pytest.approx(nvl["user_bytes"] * 16 / 128, rel=1e-5)
+    assert nvl["nvltx_bytes"] == pytest.approx(nvl["user_bytes"] * 24 / 128, abs=128)   # + the credit
+    assert 900 * nvl["user_bytes"] / nvl["nvlrx_bytes"] == pytest.approx(800.0, rel=1e-5)
+    assert 900 * nvl["user_bytes"] / (nvl["nvlrx_bytes"] + nvl["nvltx_bytes"]) == pytest.approx(685.7, rel=1e-3)
