@@ -9,6 +9,7 @@
 #   n4c   (4 GPUs) 8-rank bench rehearsal, gather, 4-rank multi tests
 #   partition  (2 GPUs) NEXT-3 planner vs measured for 16-16 / 15-17 / 14-18
 #   final2  (2 GPUs) final build: N=2 line, 500-step stability, NVLink counters, C5 sweep
+#   final4  (4 GPUs) final build: N=8 bench rehearsal (8 ranks on 4 GPUs), exposure at 1 block/stage
 # Logs: gpurun_out/TAG_*.  Copies of the judged ones are in profiles/round2/.
 PASS=$1; T=${2:-$1}
 mkdir -p gpurun_out
@@ -121,8 +122,20 @@ pass_final2() {
   tail -n 2 gpurun_out/${T}_sweep.log
 }
 
+# final (4 GPUs): the N=8 bench path rehearsed (8 ranks, 2 per GPU), exposure at 1 block per
+# stage (PP2, PP2 x TP2 with NCCL, PP4) on the final build
+pass_final4() {
+  timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 8 --master-addr 127.0.0.1 \
+    --master-port 29411 bench.py --gpus 8 --steps 5 --warmup 3 > gpurun_out/${T}_bench8_rehearsal.log 2>&1
+  echo "rc=$?"; grep '^{"metric' gpurun_out/${T}_bench8_rehearsal.log | cut -c1-300
+  trun 2 bench_exposure.py --layers 1 --reps 5 --out gpurun_out/${T}_exposure.jsonl > gpurun_out/${T}_exp_pp2.log 2>&1
+  trun 4 bench_exposure.py --pp 2 --tp 2 --M 16 --layers 1 --reps 5 --out gpurun_out/${T}_exposure.jsonl > gpurun_out/${T}_exp_pp2tp2.log 2>&1
+  trun 4 bench_exposure.py --pp 4 --M 16 --layers 1 --reps 5 --out gpurun_out/${T}_exposure.jsonl > gpurun_out/${T}_exp_pp4.log 2>&1
+  cut -c1-300 gpurun_out/${T}_exposure.jsonl
+}
+
 case $PASS in
-  n2|n2b|n2c|n4|n4b|n4c|partition|final2) pass_$PASS ;;
-  *) echo "usage: tools/perf.sh n2|n2b|n2c|n4|n4b|n4c|partition|final2 [TAG]"; exit 2 ;;
+  n2|n2b|n2c|n4|n4b|n4c|partition|final2|final4) pass_$PASS ;;
+  *) echo "usage: tools/perf.sh n2|n2b|n2c|n4|n4b|n4c|partition|final2|final4 [TAG]"; exit 2 ;;
 esac
 true
