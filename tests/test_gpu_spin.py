@@ -220,7 +220,8 @@ def test_per_rank_step_driver_xor(engine, S, M, K):
     _close(comms)
 
 
-@pytest.mark.parametrize("mode", ["fused", "unfused", "side", "early", "batch"])
+@pytest.mark.parametrize("mode", ["fused", "unfused", "side", "early", "batch", "nochain",
+                                  "lastworker", "static"])
 def test_zero_copy_publication_and_pull(mode, monkeypatch):
     """Registered send buffers: the sender only publishes (segment, offset) in the receiver's
     slot header, the receiver pulls the payload straight into its buffer.  Ragged messages
@@ -230,9 +231,14 @@ def test_zero_copy_publication_and_pull(mode, monkeypatch):
     publication kernel (PPC_FUSE_PUBLISH=0); side: publication on the send stream
     (PPC_ZC_SIDE=1); early: receives look for the publication before griddepcontrol.wait
     (PPC_RECV_EARLY=1); batch: the step's terminal receives with their fused publications
-    as one batched-receive grid (PPC_STEP_BATCH=1)."""
+    as one batched-receive grid (PPC_STEP_BATCH=1); the fallbacks of the final per-hop
+    changes: nochain (PPC_RECV_CHAIN=0: every receive waits at griddepcontrol.wait),
+    lastworker (PPC_PUB_BLOCK0=0: the last worker releases the fused publication behind its
+    own system fence), static (PPC_PULL_DYN=0: static chunk ranges per CTA)."""
     env = {"unfused": ("PPC_FUSE_PUBLISH", "0"), "side": ("PPC_ZC_SIDE", "1"),
-           "early": ("PPC_RECV_EARLY", "1"), "batch": ("PPC_STEP_BATCH", "1")}
+           "early": ("PPC_RECV_EARLY", "1"), "batch": ("PPC_STEP_BATCH", "1"),
+           "nochain": ("PPC_RECV_CHAIN", "0"), "lastworker": ("PPC_PUB_BLOCK0", "0"),
+           "static": ("PPC_PULL_DYN", "0")}
     if mode in env:
         monkeypatch.setenv(*env[mode])
     comms = _comms(max_msg_bytes=8 << 20, chunk_bytes=256 << 10, trace=1)
@@ -330,12 +336,26 @@ def test_zero_copy_async_stream():
 @pytest.mark.parametrize("S", [2, 3])
 @pytest.mark.parametrize("zc", [False, True])
 def test_per_rank_cuda_graph(S, zc, batch, monkeypatch):
+    _per_rank_cuda_graph(S, zc, batch, "default", monkeypatch)
+
+
+@pytest.mark.parametrize("S", [2, 3])
+def test_per_rank_cuda_graph_legacy_hops(S, monkeypatch):
+    _per_rank_cuda_graph(S, True, 0, "legacy", monkeypatch)
+
+
+def _per_rank_cuda_graph(S, zc, batch, hop, monkeypatch):
     """Each rank's step captured into its own CUDA graph (ppc_graph_create with n = 1, the
     one-process-per-GPU form; device-side sequence bases), replayed interleaved with eager
     steps.  zc: identity stages with registered X / G (zero-copy pulls and the fused
     publication inside the graphs); otherwise XOR stages over the ring.  batch: terminal
-    receives as one batched-receive grid per step (PPC_STEP_BATCH=1)."""
+    receives as one batched-receive grid per step (PPC_STEP_BATCH=1).  legacy: without the
+    final per-hop changes (no chained receives, last-worker publication, static pull ranges);
+    default: with them (chained receives resolve their predecessor's seq on the device)."""
     monkeypatch.setenv("PPC_STEP_BATCH", str(batch))
+    if hop == "legacy":
+        for k in ("PPC_RECV_CHAIN", "PPC_PUB_BLOCK0", "PPC_PULL_DYN"):
+            monkeypatch.setenv(k, "0")
     M, n = 4, 3 * (256 << 10) + 99
     comms = _comms(pp=S, max_msg_bytes=n, chunk_bytes=256 << 10)
     args, X, G, Y, DX = _xor_args(comms, S, M, n, fn=not zc)
