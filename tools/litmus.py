@@ -75,13 +75,17 @@ def main():
     torch.cuda.synchronize()
     t_run = time.perf_counter() - t0
     errors = [ppc.STATUS[c.poll()] for c in comms if c.poll()]
-    # device-side verification, 20k messages at a time: gather the expected bytes
+    # device-side verification, at most 20k messages / 512 MiB at a time (the gather index
+    # tensors stay far below 2^31 elements): gather the expected bytes
     bad = 0
     for d in (0, 1):
-        for a0 in range(0, per_dir, 20_000):
-            a1 = min(per_dir, a0 + 20_000)
-            sz = torch.from_numpy(sizes[d][a0:a1]).cuda()
-            of = torch.from_numpy(offs[d][a0:a1]).cuda()
+        a0 = 0
+        while a0 < per_dir:
+            a1 = min(per_dir, a0 + 20_000,
+                     int(np.searchsorted(cum[d], cum[d][a0] + (512 << 20), side="right")) - 1)
+            lo, a0 = a0, max(a1, a0 + 1)
+            sz = torch.from_numpy(sizes[d][lo:a0]).cuda()
+            of = torch.from_numpy(offs[d][lo:a0]).cuda()
             tot = int(sz.sum())
             if tot == 0:
                 continue
@@ -89,7 +93,7 @@ def main():
             first = torch.cumsum(sz, 0) - sz
             within = torch.arange(tot, device="cuda") - torch.repeat_interleave(first, sz)
             want = src[d][starts + within]
-            got = logs[d][int(cum[d][a0]):int(cum[d][a0]) + tot]
+            got = logs[d][int(cum[d][lo]):int(cum[d][lo]) + tot]
             bad += int((want != got).sum())
     rec = {"messages": 2 * per_dir, "bytes": int(sum(c[-1] for c in cum)), "zero_copy": a.zc,
            "K": a.K, "chunk": a.chunk, "max_bytes": a.max_bytes, "mismatching_bytes": bad,
