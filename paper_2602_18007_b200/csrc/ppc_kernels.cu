@@ -192,12 +192,19 @@ __device__ __forceinline__ uint64_t dbg_stamp_sm() {
 }
 
 // Wait until *p >= target (wrap-safe); false on timeout.
+// A latched error poisons the comm (ErrWord): every other bounded wait of the comm gives up
+// at its next check instead of running into its own deadline, so one failure does not
+// cost one timeout per queued kernel.
+__device__ __forceinline__ bool err_claimed(const ErrWord* e) {
+  return e && *reinterpret_cast<const volatile unsigned*>(&e->claim) != 0u;
+}
 template <bool kSys = true>
-__device__ __forceinline__ bool wait_geq(const uint64_t* p, uint64_t target, uint64_t deadline) {
+__device__ __forceinline__ bool wait_geq(const uint64_t* p, uint64_t target, uint64_t deadline,
+                                         const ErrWord* err) {
   uint64_t v = ld_acq<kSys>(p);
   int spins = 0;
   while ((int64_t)(v - target) < 0) {
-    if (((++spins) & 63) == 0 && globaltimer() > deadline) return false;
+    if (((++spins) & 63) == 0 && (globaltimer() > deadline || err_claimed(err))) return false;
     __nanosleep(32);
     v = ld_acq<kSys>(p);
   }
@@ -343,7 +350,7 @@ __global__ void __launch_bounds__(kThreads) push_kernel(PushArgs a0) {
     deadline = t0 + a.timeout_ns;
     if (a.rec && blockIdx.x == 0)
       fill_record(a.rec, (long long)t0, a.rec_src, a.rec_dst, a.dir, 0, a.seq, a.mb, a.bytes);
-    if (a.need_credit && !wait_geq<kSys>(a.credit, a.need_credit, deadline)) {
+    if (a.need_credit && !wait_geq<kSys>(a.credit, a.need_credit, deadline, a.err)) {
       latch(a.err, PPC_ERR_TIMEOUT, a.seq, a.dir);
       fail = 1;
     } else if (blockIdx.x == 0) {
@@ -433,7 +440,7 @@ __global__ void __launch_bounds__(kWsThreads) push_ws_kernel(PushArgs a0) {
       mbar_init(&empty[b], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (a.need_credit && !wait_geq<kSys>(a.credit, a.need_credit, deadline)) {
+    if (a.need_credit && !wait_geq<kSys>(a.credit, a.need_credit, deadline, a.err)) {
       latch(a.err, PPC_ERR_TIMEOUT, a.seq, a.dir);
       fail = 1;
     } else if (blockIdx.x == 0) {
@@ -495,7 +502,7 @@ __global__ void __launch_bounds__(kWsThreads) push_ws_kernel(PushArgs a0) {
 // Flag phase: st.release.sys of the header flag (cumulative over the header and over the
 // producer's writes to the buffer).  false = the credit wait timed out (error latched).
 __device__ __forceinline__ bool publish_header(const PublishArgs& a) {
-  if (a.need_credit && !wait_geq(a.credit, a.need_credit, globaltimer() + a.timeout_ns)) {
+  if (a.need_credit && !wait_geq(a.credit, a.need_credit, globaltimer() + a.timeout_ns, a.err)) {
     latch(a.err, PPC_ERR_TIMEOUT, a.seq, a.dir);
     return false;
   }
@@ -615,7 +622,7 @@ __device__ __forceinline__ bool chain_enter(const RecvArgs& a0) {
   int fail = 0;
   if (threadIdx.x == 0) {
     const uint64_t target = a0.chain_seq + (a0.chain_base ? *a0.chain_base : 0);
-    if (!wait_geq<false>(a0.chain_wait, target, globaltimer() + a0.timeout_ns)) {
+    if (!wait_geq<false>(a0.chain_wait, target, globaltimer() + a0.timeout_ns, a0.err)) {
       latch(a0.err, PPC_ERR_TIMEOUT, a0.seq, 0x700u);
       fail = 1;
     }
@@ -625,13 +632,14 @@ __device__ __forceinline__ bool chain_enter(const RecvArgs& a0) {
   return !fail;
 }
 // block 0 of a kPub receive: wait (bounded) until the n worker CTAs have arrived
-__device__ __forceinline__ bool wait_arrivals(const uint32_t* done, uint32_t n, uint64_t deadline) {
+__device__ __forceinline__ bool wait_arrivals(const uint32_t* done, uint32_t n, uint64_t deadline,
+                                              const ErrWord* err) {
   int spins = 0;
   for (;;) {
     uint32_t v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(done) : "memory");
     if (v >= n) return true;
-    if (((++spins) & 255) == 0 && globaltimer() > deadline) return false;
+    if (((++spins) & 255) == 0 && (globaltimer() > deadline || err_claimed(err))) return false;
   }
 }
 // end of a receive's data phase (its last CTA, after the done count): post its seq
@@ -713,7 +721,7 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(const __grid_constant__ 
     // before the flag the last CTA releases (ordered after us through the done counter)
     if (kPub && blockIdx.x == 0 && !fused_publish_header(&a0.pub)) fail = 1;
     if (fail) {
-    } else if (!wait_geq<kSys>(a.hdr_flag, a.seq, deadline)) {
+    } else if (!wait_geq<kSys>(a.hdr_flag, a.seq, deadline, a.err)) {
       latch(a.err, PPC_ERR_TIMEOUT, a.seq, 0x100u);
       fail = 1;
     } else {
@@ -786,7 +794,7 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(const __grid_constant__ 
       continue;
     }
     int f = 0;
-    if (threadIdx.x == 0 && !wait_geq<kSys>(a.flags + c, a.seq, deadline)) {
+    if (threadIdx.x == 0 && !wait_geq<kSys>(a.flags + c, a.seq, deadline, a.err)) {
       latch(a.err, PPC_ERR_TIMEOUT, a.seq, 0x100u | c << 12);
       f = 1;
     }
@@ -805,7 +813,7 @@ __global__ void __launch_bounds__(kThreads) recv_kernel(const __grid_constant__ 
     // arrival; the published payload was written by earlier kernels.
     if (blockIdx.x != 0) {
       atomicAdd(a.done, 1u);
-    } else if (!wait_arrivals(a.done, gridDim.x - 1, deadline)) {
+    } else if (!wait_arrivals(a.done, gridDim.x - 1, deadline, a.err)) {
       latch(a.err, PPC_ERR_TIMEOUT, a.seq, 0x800u);
     } else {
       *a.done = 0;                 // next use of this slot is stream-ordered after us
@@ -866,7 +874,7 @@ __global__ void __launch_bounds__(kThreads) recv_batch_kernel(const __grid_const
         fill_record(a.rec, (long long)t0, a.rec_src, a.rec_dst, -1, 1, a.seq, a.mb, a.bytes);
       if (kPub && blockIdx.x == 0 && a.has_pub && !fused_publish_header(&b.a[i].pub)) {
         fail = 1;
-      } else if (!wait_geq<kSys>(a.hdr_flag, a.seq, deadline)) {
+      } else if (!wait_geq<kSys>(a.hdr_flag, a.seq, deadline, a.err)) {
         latch(a.err, PPC_ERR_TIMEOUT, a.seq, 0x100u);
         fail = 1;
       } else {
@@ -906,7 +914,7 @@ __global__ void __launch_bounds__(kThreads) recv_batch_kernel(const __grid_const
           continue;
         }
         int f = 0;
-        if (threadIdx.x == 0 && !wait_geq<kSys>(a.flags + c, a.seq, deadline)) {
+        if (threadIdx.x == 0 && !wait_geq<kSys>(a.flags + c, a.seq, deadline, a.err)) {
           latch(a.err, PPC_ERR_TIMEOUT, a.seq, 0x100u | c << 12);
           f = 1;
         }
@@ -970,7 +978,7 @@ __global__ void __launch_bounds__(kThreads) gather_kernel(GatherArgs a) {
     if (need) {
       int fail = 0;
       if (threadIdx.x == 0) {
-        if (!wait_geq<true>(a.hdr_flag[t], a.seq, deadline)) {
+        if (!wait_geq<true>(a.hdr_flag[t], a.seq, deadline, a.err)) {
           latch(a.err, PPC_ERR_TIMEOUT, a.seq, 0x400u | t << 12);
           fail = 1;
         } else {
@@ -1017,7 +1025,7 @@ __global__ void gather_credit_kernel(const unsigned long long* gdone, uint64_t g
                                      uint64_t timeout_ns) {
   pdl_enter();
   if (!wait_geq<true>(reinterpret_cast<const uint64_t*>(gdone), gtarget,
-                      globaltimer() + timeout_ns)) {
+                      globaltimer() + timeout_ns, err)) {
     latch(err, PPC_ERR_TIMEOUT, seq, 0x600u);
     return;
   }
@@ -1053,7 +1061,7 @@ __global__ void ce_head_kernel(CeHeadArgs a) {
   pdl_enter();
   const uint64_t t0 = globaltimer();
   if (a.rec) fill_record(a.rec, (long long)t0, a.rec_src, a.rec_dst, a.dir, 0, a.seq, a.mb, a.bytes);
-  if (a.need_credit && !wait_geq(a.credit, a.need_credit, t0 + a.timeout_ns)) {
+  if (a.need_credit && !wait_geq(a.credit, a.need_credit, t0 + a.timeout_ns, a.err)) {
     latch(a.err, PPC_ERR_TIMEOUT, a.seq, a.dir);
     return;
   }
@@ -1086,7 +1094,7 @@ __global__ void wait_credit_kernel(const uint64_t* credit, uint64_t target, ErrW
                                    uint64_t timeout_ns, const uint64_t* seq_base) {
   pdl_enter();
   if (seq_base) target += *seq_base;
-  if (!wait_geq(credit, target, globaltimer() + timeout_ns)) latch(err, PPC_ERR_TIMEOUT, target, 0x200u);
+  if (!wait_geq(credit, target, globaltimer() + timeout_ns, err)) latch(err, PPC_ERR_TIMEOUT, target, 0x200u);
 }
 
 __global__ void set_seq_kernel(uint64_t* seq, uint64_t v0, uint64_t v1, uint64_t v2, uint64_t v3) {

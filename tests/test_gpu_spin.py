@@ -8,6 +8,8 @@ seeded inputs (synth/payload.py), bit-exact.  tests/test_gpu_multi.py runs the s
 across processes (ranks share the GPU when fewer GPUs than ranks are visible)."""
 import hashlib
 
+import time
+
 import numpy as np
 import pytest
 import torch
@@ -142,6 +144,27 @@ def test_header_errors_on_device():
     comms[1].recv(ppc.FWD, dst, 4096, mb=4, stream=s1)
     torch.cuda.synchronize()
     assert comms[1].error_info()[:2] == ("ORDER", 1)
+    _close(comms, expect_ok=False)
+
+
+def test_latched_error_aborts_queued_waits():
+    """One failure poisons the comm and every other bounded wait of it gives up at its next
+    check: after a header ORDER error, three more receives queued on the same stream (whose
+    messages never come) end within a fraction of their 3 s timeout each, and the latched
+    record stays the first failure's."""
+    comms = _comms(max_msg_bytes=1 << 20, timeout_ns=3_000_000_000)
+    s0, s1 = torch.cuda.Stream(), torch.cuda.Stream()
+    src = _buf(4096)
+    dst = [_buf(4096) for _ in range(4)]
+    comms[0].send(ppc.FWD, src, 4096, mb=3, stream=s0)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(4):                     # mb=4 mismatches the sent mb=3: ORDER on the first
+        comms[1].recv(ppc.FWD, dst[i], 4096, mb=4 + i, stream=s1)
+    torch.cuda.synchronize()
+    elapsed = time.perf_counter() - t0
+    assert comms[1].error_info()[:2] == ("ORDER", 1)
+    assert elapsed < 1.5, elapsed           # not 3 x 3 s of timeouts
     _close(comms, expect_ok=False)
 
 
