@@ -25,7 +25,9 @@
  *    PPC_ERR_STATE.  Recovery = ppc_disconnect on every rank, a caller barrier,
  *    ppc_destroy, then a fresh ppc_create.
  *  - Every device wait is bounded by cfg.timeout_ns (%globaltimer); no unbounded spin
- *    (§4.3: "training frequently encountered hang issues").
+ *    (§4.3: "training frequently encountered hang issues").  Once an
+ *    error is latched on a comm, its other device waits give up at their next check
+ *    instead of each running into its own timeout.
  *
  * Environment (read by ppc_create / the step driver; defaults are the measured best,
  * DESIGN.md §6-7):

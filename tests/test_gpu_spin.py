@@ -156,11 +156,11 @@ def test_latched_error_aborts_queued_waits():
     s0, s1 = torch.cuda.Stream(), torch.cuda.Stream()
     src = _buf(4096)
     dst = [_buf(4096) for _ in range(4)]
-    comms[0].send(ppc.FWD, src, 4096, mb=3, stream=s0)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for i in range(4):                     # mb=4 mismatches the sent mb=3: ORDER on the first
+    for i in range(4):                     # all queued before anything fails
         comms[1].recv(ppc.FWD, dst[i], 4096, mb=4 + i, stream=s1)
+    comms[0].send(ppc.FWD, src, 4096, mb=3, stream=s0)   # mb 3 != 4: ORDER on the first
     torch.cuda.synchronize()
     elapsed = time.perf_counter() - t0
     assert comms[1].error_info()[:2] == ("ORDER", 1)
