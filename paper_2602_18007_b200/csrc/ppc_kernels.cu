@@ -600,8 +600,6 @@ __device__ __forceinline__ void fused_publish_flag(const PublishArgs* p0, uint64
   }
 }
 
-// kPub: the variant with the fused publication (step driver, terminal receives of a
-// comm-only PP2 step).  Both variants need ~90 registers: one 512-thread CTA per SM.
 // mapped base of a zero-copy source segment on this GPU; 0 if never imported
 __device__ __forceinline__ uint64_t zc_base(const RecvArgs& a, uint32_t seg) {
   return seg == kArenaSeg ? (uint64_t)(uintptr_t)a.peer_arena
@@ -648,6 +646,8 @@ __device__ __forceinline__ void chain_post(const RecvArgs& a) {
     atomicMax(reinterpret_cast<unsigned long long*>(a.chain_post), (unsigned long long)a.seq);
 }
 
+// kPub: the variant with the fused publication (step driver, terminal receives of a
+// comm-only PP2 step).  Both variants need ~90 registers: one 512-thread CTA per SM.
 template <bool kSys, bool kPub, bool kEarly = false>
 __global__ void __launch_bounds__(kThreads) recv_kernel(const __grid_constant__ RecvArgs a0) {
   __shared__ const uint8_t* s_zc_src;   // zero-copy: the sender's buffer, mapped here
