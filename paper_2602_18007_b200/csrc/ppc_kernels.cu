@@ -900,9 +900,22 @@ __global__ void __launch_bounds__(kThreads) recv_batch_kernel(const __grid_const
     if (__syncthreads_or(fail)) return;
     if (dbg && threadIdx.x == 0) dbg[1] = globaltimer();
     const uint8_t* zc_src = s_zc_src;
-    // rotate the chunk ownership per message so the CTAs that carried the last chunks of
-    // one message start the next one early
-    if (blockIdx.x >= w0) {
+    if (blockIdx.x >= w0 && zc_src && a.dyn) {
+      // dynamic pull units (PPC_PULL_DYN, as recv_kernel): warps claim 4 KiB units of
+      // message i; a CTA whose warps find none left moves on to message i + 1
+      const uint32_t lane = threadIdx.x & 31;
+      const uint64_t n_units = (a.bytes + kPullUnit - 1) / kPullUnit;
+      uint32_t u = lane == 0 ? atomicAdd(a.next, 1u) : 0u;
+      u = __shfl_sync(0xffffffffu, u, 0);
+      while (u < n_units) {
+        const uint32_t nx = lane == 0 ? atomicAdd(a.next, 1u) : 0u;
+        const uint64_t off = (uint64_t)u * kPullUnit;
+        cta_copy<true>(a.dst + off, zc_src + off, min((uint64_t)kPullUnit, a.bytes - off), lane, 32);
+        u = __shfl_sync(0xffffffffu, nx, 0);
+      }
+    } else if (blockIdx.x >= w0) {
+      // rotate the chunk ownership per message so the CTAs that carried the last chunks of
+      // one message start the next one early
       const uint32_t wid = blockIdx.x - w0;
       const uint32_t first = (wid + i * (a.n_chunks % workers)) % workers;
       for (uint32_t c = first; c < a.n_chunks; c += workers) {
@@ -928,6 +941,7 @@ __global__ void __launch_bounds__(kThreads) recv_batch_kernel(const __grid_const
     if (threadIdx.x == 0) {
       if (atomicAdd(a.done, 1u) == gridDim.x - 1) {
         *a.done = 0;
+        *a.next = 0;
         __threadfence();
         chain_post(a);
         if (kPub && a.has_pub) {
