@@ -477,9 +477,10 @@ def connect_distributed(cfg: Config, rank: int, world: int, device: int, pg=None
         mine = {}
         tp_m, _ = comm.group(GROUP_TP)
         dp_m, _ = comm.group(GROUP_DP)
-        if rank == min(tp_m) and len(tp_m) > 1:
+        single = os.environ.get("PPC_NCCL_SINGLETON") == "1"   # tests: one-rank groups too
+        if rank == min(tp_m) and (len(tp_m) > 1 or single):
             mine["tp"] = nccl_unique_id()
-        if rank == min(dp_m) and len(dp_m) > 1:
+        if rank == min(dp_m) and (len(dp_m) > 1 or single):
             mine["dp"] = nccl_unique_id()
         allids = [None] * world
         dist.all_gather_object(allids, mine, group=pg)

@@ -401,7 +401,13 @@ ppc_status_t ppc_connect(ppc_comm_t* c, const void* all_blobs, size_t blob_bytes
     const ncclUniqueId* ids = static_cast<const ncclUniqueId*>(nccl_ids);
     for (int gi = 0; gi < n_ids; ++gi) {
       const std::vector<int>& mem = c->members[gi];
-      if (mem.size() < 2) continue;
+      // PPC_NCCL_SINGLETON=1 (tests): a one-rank group gets its own one-rank communicator
+      // too, so the NCCL init and allreduce path runs where ranks share one GPU (NCCL
+      // refuses two ranks of one communicator on one GPU); a zero id = no communicator
+      static const ncclUniqueId kZero{};
+      if (mem.size() < 2 && (!env_int("PPC_NCCL_SINGLETON", 0) ||
+                             memcmp(&ids[gi], &kZero, sizeof(kZero)) == 0))
+        continue;
       const int r = (int)(std::find(mem.begin(), mem.end(), c->rank) - mem.begin());
       if (ncclCommInitRank(&c->nccl[gi], (int)mem.size(), ids[gi], r) != ncclSuccess)
         return PPC_ERR_NCCL;
@@ -956,7 +962,8 @@ ppc_status_t ppc_allreduce(ppc_comm_t* c, ppc_group_t g, void* buf, size_t count
   if (g == PPC_GROUP_PP) return PPC_ERR_BACKEND;      // DCBS: PP is not a collective group
   if (g != PPC_GROUP_TP && g != PPC_GROUP_DP) return PPC_ERR_INVALID_ARG;
   if (count && !buf) return PPC_ERR_INVALID_ARG;
-  if (c->members[g].size() < 2 || count == 0) return PPC_OK;    // group of one: identity
+  if (count == 0) return PPC_OK;
+  if (c->members[g].size() < 2 && !c->nccl[g]) return PPC_OK;    // group of one: identity
   if (!c->nccl[g]) return PPC_ERR_STATE;
   DeviceGuard gd(c->device);
   if (ncclAllReduce(buf, buf, count, (ncclDataType_t)nccl_dtype, ncclSum, c->nccl[g], s) !=

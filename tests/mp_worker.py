@@ -149,6 +149,51 @@ def case_timeout(rank, world):
     return comm
 
 
+def case_dcbs1(rank, world):
+    """DCBS with one-rank TP / DP groups, ranks sharing a GPU (the driver's one-GPU box):
+    under PPC_NCCL_SINGLETON=1 every group still gets its own NCCL communicator, so the id
+    exchange, ncclCommInitRank and ncclAllReduce run through the C ABI beside the PP kernels
+    of a 1F1B step; the allreduce over a one-rank group is the identity."""
+    assert os.environ.get("PPC_NCCL_SINGLETON") == "1"
+    cfg = ppc.make_config(tp=1, pp=world, dp=1, max_msg_bytes=2 << 20)
+    comm = ppc.connect_distributed(cfg, rank, world, dev(rank), with_nccl=True)
+    tp_m, be = comm.group(ppc.GROUP_TP)
+    dp_m, be_dp = comm.group(ppc.GROUP_DP)
+    pp_m, be_pp = comm.group(ppc.GROUP_PP)
+    assert tp_m == [rank] and dp_m == [rank] and pp_m == list(range(world))
+    assert be == be_dp == ppc.BACKEND_NCCL and be_pp == ppc.BACKEND_PEER
+    side = torch.cuda.Stream()
+    t = torch.full((1 << 20,), float(rank + 1), device="cuda")
+    with torch.cuda.stream(side):
+        comm.allreduce(ppc.GROUP_TP, t, 7, stream=side)        # ncclFloat32 = 7
+        comm.allreduce(ppc.GROUP_DP, t, 7, stream=side)
+    try:
+        comm.allreduce(ppc.GROUP_PP, t, 7)
+        raise AssertionError("PP allreduce must be refused (DCBS)")
+    except ppc.PpcError as e:
+        assert e.name == "BACKEND"
+    n, M = (1 << 20) + 3, 4
+    X = [buf(n) for _ in range(M)] if rank == 0 else None
+    G = [buf(n) for _ in range(M)] if rank == world - 1 else None
+    for m in range(M):
+        if X:
+            ppc.fill_payload(X[m], n, 42, 0, P.SRC_BOUNDARY, 0, m)
+        if G:
+            ppc.fill_payload(G[m], n, 42, 0, P.SRC_BOUNDARY, 1, m)
+    torch.cuda.synchronize()
+    out = [buf(n) for _ in range(M)]
+    args = ppc.StepArgs(M, n, n, x=X, g=G, y=out if G else None, dx=out if X else None)
+    ppc.step_1f1b(comm, args, torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    assert comm.poll() == 0
+    assert torch.all(t == float(rank + 1)).item()
+    for m in range(M):      # identity stages: stage 0 gets G_m back, last stage gets X_m
+        if X or G:
+            ref = P.source_gradient(42, 0, m, n) if X else P.source_activation(42, 0, m, n)
+            assert np.array_equal(host(out[m])[:n], ref)
+    return comm
+
+
 def case_dcbs(rank, world):
     """PP=2 x TP=2 on 4 GPUs: TP allreduce on NCCL running beside the PP kernels."""
     tp = 2
@@ -590,6 +635,8 @@ def main():
         comm = case_gather(rank, world)
     elif case == "dcbs":
         comm = case_dcbs(rank, world)
+    elif case == "dcbs1":
+        comm = case_dcbs1(rank, world)
     else:
         raise SystemExit(f"unknown case {case}")
     torch.cuda.synchronize()

@@ -60,6 +60,14 @@ def test_dcbs_pp2_tp2():
     _run("dcbs", 4)
 
 
+@pytest.mark.parametrize("n", [2, 3])
+def test_dcbs_nccl_singleton_groups(n):
+    """DCBS group init with NCCL communicators that any box can build (one-rank TP / DP
+    groups; the ranks may share one GPU): NCCL init + allreduce through the C ABI beside a
+    PP step, PP collectives refused."""
+    _run("dcbs1", n, env={"PPC_NCCL_SINGLETON": "1"})
+
+
 @pytest.mark.parametrize("n", [2, 4])
 def test_hetero_allreduce(n):
     _run("hetero", n)
