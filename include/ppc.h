@@ -69,6 +69,9 @@
  *                        cuStreamWaitValue64 instead of the bounded 1-thread kernel: zero SMs,
  *                        but UNBOUNDED (no timeout) — measured opt-in, DESIGN.md §7
  *   PPC_XOR_SEND_CTAS=296  grid cap of the fused XOR-send kernel
+ *   PPC_SPIN_GRID_CAP=64 cap of cross-GPU spinning grids (receive / push / gather); larger
+ *                        grids are safe since kernels are preloaded, 64 is the fastest
+ *   PPC_NCCL_SINGLETON=0 tests: one-rank TP / DP groups get one-rank NCCL communicators too
  *   PPC_RECV_CTAS, PPC_STAGE_CTAS, PPC_PUSH_WS=1   grid / kernel-variant overrides
  */
 #ifndef PPC_H_

@@ -170,6 +170,8 @@ ppc_status_t ppc_create(const ppc_config_t* cfg, int world, int rank, int cuda_d
   ppc::g_recv_early = env_int("PPC_RECV_EARLY", 0) != 0 ? 1 : 0;
   ppc::g_copy_tma_ctas = std::max(0, env_int("PPC_COPY_TMA_CTAS", 0));
   ppc::g_wait_value = env_int("PPC_WAIT_VALUE", 0) != 0 ? 1 : 0;
+  ppc::kMaxSpinGrid = std::max(1, env_int("PPC_SPIN_GRID_CAP", 64));
+  c->spin_cap = ppc::kMaxSpinGrid;
   const int tp = cfg->tp, dp = cfg->dp;
   c->pp_i = rank / (tp * dp);
   c->dp_i = (rank % (tp * dp)) / tp;

@@ -211,6 +211,7 @@ cudaError_t preload_kernels();
 // launch transport kernels with programmatic dependent launch (ppc_kernels.cu); set from
 // PPC_PDL by ppc_create
 extern int g_pdl;
+extern int kMaxSpinGrid;   // cap of cross-GPU spinning grids (64; PPC_SPIN_GRID_CAP)
 extern int g_copy_tma_ctas;
 extern int g_wait_value;       // PPC_WAIT_VALUE: eager credit waits as cuStreamWaitValue64
 extern std::atomic<unsigned long long> g_launches;   // ppc_launch_count

@@ -80,13 +80,14 @@ int fit_grid(void (*k)(KArgs...), int grid, unsigned block) {
   const unsigned cap = resident_capacity(k, block);
   return (cap && (unsigned)grid > cap) ? (int)cap : grid;
 }
-// Cross-GPU spinning receives (and their PDL successor) must also leave SMs free for the
-// 1-thread publication / credit kernels the peer is waiting on.  Measured (2 x B200,
-// tools/zc_bidir.py, profiles/r47_zc_bidir.log): a bidirectional zero-copy stream runs with
-// 64-CTA receive grids (+ the PDL successor = 128 CTAs) and stalls until the timeout as
-// soon as the receive CTAs in flight exceed the SM count (96 + 96, 128 + 128, 256), although
-// the occupancy calculator allows two of these CTAs per SM.  64 CTAs pull at full speed.
-constexpr int kMaxSpinGrid = 64;
+// Cap of cross-GPU spinning grids.  Round 1 measured a bidirectional zero-copy stream
+// stalling once the receive CTAs in flight exceeded the SM count (profiles/r47_zc_bidir.log);
+// the cause was a lazy module load waiting for an idle device behind spinning receives
+// (ppc_create now preloads every kernel): the same stream runs clean with 96, 128, 148 and
+// 256-CTA grids, with and without PDL (profiles/round2/p44_zc_bidir_grids/).  64 stays the
+// default because it is the fastest grid for pulls with both directions loaded
+// (profiles/round2/p24_bidir_probe.jsonl: 596 GB/s at 64 vs 556-560 at 96 / 148).
+int kMaxSpinGrid = 64;   // PPC_SPIN_GRID_CAP
 
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(void (*k)(KArgs...), unsigned grid, unsigned block, cudaStream_t s,
