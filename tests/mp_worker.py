@@ -584,68 +584,82 @@ def case_inplace(rank, world, M=6):
     return comm
 
 
-def main():
-    case = sys.argv[1]
-    rank = int(os.environ["RANK"])
-    world = int(os.environ["WORLD_SIZE"])
-    torch.cuda.set_device(dev(rank))
-    dist.init_process_group("gloo")
-    if case == "sendrecv_sm":
-        comm = case_sendrecv(rank, world, ppc.ENGINE_SM)
-    elif case == "sendrecv_ce":
-        comm = case_sendrecv(rank, world, ppc.ENGINE_CE)
-    elif case == "xor_sm":
-        comm = case_xor(rank, world, ppc.ENGINE_SM)
-    elif case == "xor_ce":
-        comm = case_xor(rank, world, ppc.ENGINE_CE)
-    elif case == "xor_pull":
-        comm = case_xor(rank, world, ppc.ENGINE_PULL)
-    elif case == "sendrecv_pull":
-        comm = case_sendrecv(rank, world, ppc.ENGINE_PULL)
-    elif case == "timeout":
-        comm = case_timeout(rank, world)
-    elif case == "toy":
-        comm = case_toy(rank, world)
-    elif case == "hetero":
-        comm = case_hetero(rank, world)
-    elif case == "zc":
-        comm = case_zc(rank, world)
-    elif case == "zc_unfused":           # publication by its own kernel (PPC_FUSE_PUBLISH=0)
-        os.environ["PPC_FUSE_PUBLISH"] = "0"
-        comm = case_zc(rank, world)
-    elif case == "zc_side":              # publication on the send stream (PPC_ZC_SIDE=1)
-        os.environ["PPC_ZC_SIDE"] = "1"
-        comm = case_zc(rank, world)
-    elif case == "zc_bidir_stream":
-        comm = case_zc_bidir_stream(rank, world)
-    elif case == "host":
-        comm = case_host(rank, world)
-    elif case == "zc_async":
-        comm = case_zc_async(rank, world)
-    elif case == "graph":
-        comm = case_graph(rank, world)
-    elif case == "xor_inplace":           # the step's stage fns produce into the slot
-        os.environ["PPC_STEP_INPLACE"] = "1"
-        comm = case_xor(rank, world, ppc.ENGINE_SM)
-    elif case == "inplace":
-        comm = case_inplace(rank, world)
-    elif case == "fullsize":
-        comm = case_fullsize(rank, world)
-    elif case == "gather":
-        comm = case_gather(rank, world)
-    elif case == "dcbs":
-        comm = case_dcbs(rank, world)
-    elif case == "dcbs1":
-        comm = case_dcbs1(rank, world)
-    else:
+CASES = {
+    "sendrecv_sm": lambda r, w: case_sendrecv(r, w, ppc.ENGINE_SM),
+    "sendrecv_ce": lambda r, w: case_sendrecv(r, w, ppc.ENGINE_CE),
+    "sendrecv_pull": lambda r, w: case_sendrecv(r, w, ppc.ENGINE_PULL),
+    "xor_sm": lambda r, w: case_xor(r, w, ppc.ENGINE_SM),
+    "xor_ce": lambda r, w: case_xor(r, w, ppc.ENGINE_CE),
+    "xor_pull": lambda r, w: case_xor(r, w, ppc.ENGINE_PULL),
+    "timeout": case_timeout,
+    "toy": case_toy,
+    "hetero": case_hetero,
+    "zc": case_zc,
+    "zc_bidir_stream": case_zc_bidir_stream,
+    "host": case_host,
+    "zc_async": case_zc_async,
+    "graph": case_graph,
+    "inplace": case_inplace,
+    "fullsize": case_fullsize,
+    "gather": case_gather,
+    "dcbs": case_dcbs,
+    "dcbs1": case_dcbs1,
+}
+# cases that are another case under an environment setting
+VARIANTS = {
+    "zc_unfused": ("zc", {"PPC_FUSE_PUBLISH": "0"}),       # publication by its own kernel
+    "zc_side": ("zc", {"PPC_ZC_SIDE": "1"}),               # publication on the send stream
+    "xor_inplace": ("xor_sm", {"PPC_STEP_INPLACE": "1"}),  # stage fns produce into the slot
+}
+
+
+def run_case(case, rank, world):
+    """One case end to end: its comm is disconnected and destroyed before returning."""
+    if case in VARIANTS:
+        base, env = VARIANTS[case]
+        os.environ.update(env)
+        case = base
+    if case not in CASES:
         raise SystemExit(f"unknown case {case}")
+    comm = CASES[case](rank, world)
     torch.cuda.synchronize()
     dist.barrier()
     comm.disconnect()
     dist.barrier()
     comm.destroy()
+
+
+def main():
+    """mp_worker.py CASE  |  mp_worker.py --batch JSON  (JSON = [[case, {env}], ...]: the
+    cases run one after another in this process group, each with its environment set and
+    the process environment restored afterwards; '#i case OK' per case)."""
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(dev(rank))
+    dist.init_process_group("gloo")
+    if sys.argv[1] == "--batch":
+        import json
+        import traceback
+        for i, (case, env) in enumerate(json.loads(sys.argv[2])):
+            saved = dict(os.environ)
+            os.environ.update(env)
+            try:
+                run_case(case, rank, world)
+            except BaseException:
+                print(f"rank {rank} #{i} {case} FAIL", flush=True)
+                traceback.print_exc()
+                sys.stdout.flush()
+                os._exit(1)               # the other ranks may be inside a collective
+            finally:
+                for k in set(os.environ) - set(saved):
+                    del os.environ[k]
+                os.environ.update(saved)
+            print(f"rank {rank} #{i} {case} OK", flush=True)
+    else:
+        case = sys.argv[1]
+        run_case(case, rank, world)
+        print(f"rank {rank} {case} OK", flush=True)
     dist.destroy_process_group()
-    print(f"rank {rank} {case} OK", flush=True)
 
 
 if __name__ == "__main__":

@@ -2,6 +2,7 @@
 flags/credits, over NVLink when each rank has its own GPU.  With fewer GPUs than ranks the
 ranks share GPUs (time-sliced), so the whole cross-process protocol also runs on one GPU;
 only the NCCL cases that need a GPU per rank are skipped then."""
+import json
 import os
 import subprocess
 import sys
@@ -19,18 +20,56 @@ PORT = [29611]
 NEEDS_OWN_GPU = {("dcbs", 4), ("hetero", 4)}
 
 
+# Every (case, ranks, env) of this file.  The cases of one rank count run in ONE torchrun
+# session (mp_worker --batch: same checks, each case with its own comms and environment),
+# which saves a process-group start-up per case; a case the batch did not report OK is run
+# again on its own, so a batch failure can never hide or fake a result.
+PLAN = [(c, 2, {}) for c in ("sendrecv_sm", "sendrecv_ce", "sendrecv_pull", "xor_sm", "xor_ce",
+                             "xor_pull", "timeout", "toy", "inplace", "xor_inplace", "hetero",
+                             "zc", "zc_unfused", "zc_side", "zc_bidir_stream", "zc_async",
+                             "host", "graph", "fullsize")] + \
+       [(c, 2, {"PPC_RECV_EARLY": "1"}) for c in ("zc", "zc_bidir_stream", "zc_async", "graph")] + \
+       [(c, 2, {"PPC_STEP_BATCH": "1"}) for c in ("zc", "graph")] + \
+       [("dcbs1", 2, {"PPC_NCCL_SINGLETON": "1"}), ("dcbs1", 3, {"PPC_NCCL_SINGLETON": "1"})] + \
+       [(c, 4, {}) for c in ("inplace", "xor_inplace", "xor_sm", "xor_ce", "xor_pull", "hetero",
+                             "host", "graph", "fullsize", "gather", "dcbs")]
+_BATCH = {}
+
+
+def _torchrun(n, args, timeout, env=None):
+    PORT[0] += 1
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(PORT[0]),
+           os.path.join(HERE, "mp_worker.py"), *args]
+    try:
+        return subprocess.run(cmd, capture_output=True, text=True, timeout=timeout,
+                              env=None if env is None else {**os.environ, **env})
+    except subprocess.TimeoutExpired as e:
+        return subprocess.CompletedProcess(cmd, -1, e.stdout or "", e.stderr or "")
+
+
+def _batch(n):
+    """Run every planned case with n ranks in one torchrun session (once per module)."""
+    if n not in _BATCH:
+        plan = [(c, e) for c, k, e in PLAN if k == n and not
+                (torch.cuda.device_count() < n and (c, n) in NEEDS_OWN_GPU)]
+        r = _torchrun(n, ["--batch", json.dumps(plan)], timeout=120 + 40 * len(plan))
+        out = r.stdout if isinstance(r.stdout, str) else r.stdout.decode(errors="replace")
+        _BATCH[n] = {(c, json.dumps(e, sort_keys=True)): out.count(f"#{i} {c} OK") == n
+                     for i, (c, e) in enumerate(plan)}
+    return _BATCH[n]
+
+
 def _run(case, n, timeout=240, env=None):
     """torchrun n ranks of tests/mp_worker.py.  With fewer GPUs than ranks the ranks share
     the GPUs round-robin (mp_worker.dev): still one process per rank, CUDA-IPC-mapped rings,
     device flag / credit / header spins — the GPU time-slices the processes."""
     if torch.cuda.device_count() < n and (case, n) in NEEDS_OWN_GPU:
         pytest.skip(f"needs {n} GPUs (NCCL: one GPU per rank)")
-    PORT[0] += 1
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", str(PORT[0]),
-           os.path.join(HERE, "mp_worker.py"), case]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout,
-                       env=None if env is None else {**os.environ, **env})
+    key = (case, json.dumps(env or {}, sort_keys=True))
+    if os.environ.get("PPC_TEST_NO_BATCH") != "1" and _batch(n).get(key):
+        return                                   # passed inside the batch session
+    r = _torchrun(n, [case], timeout, env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count(f"{case} OK") == n
 
