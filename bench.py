@@ -838,8 +838,16 @@ def main():
                      "serialized": {"launch_us_median": us, "launches": n,
                                     "achieved": roof["alg_bytes_per_launch"] / (us * 1e-6) / 1e9,
                                     "how": "eager steps with every copy on one transfer queue "
-                                           "(PPC_LOCAL_QUEUE=1), CUDA events around each launch"},
+                                           "(PPC_LOCAL_QUEUE=1), CUDA events around each launch "
+                                           "(they add the event and launch overhead to each "
+                                           "launch; ncu_serialized is the kernel alone)"},
                      "traffic": ncu_traffic("copy_n1")})
+        ns = ncu_traffic("copy_n1_launch_ns")
+        if ns:
+            a = roof["alg_bytes_per_launch"] / (ns * 1e-9) / 1e9
+            roof["ncu_serialized"] = {"launch_us": ns * 1e-3, "achieved": a, "frac": a / roof["peak"],
+                                      "source": "committed ncu launch list of this bench "
+                                                "(profiles/ncu_traffic.json copy_n1_launch_ns)"}
     elif roof is not None and wl["zc"]:
         ph = roof.get("pull_data_phase", {})
         roof.update({"kernel": "ppc::recv_kernel (zero-copy NVLink pull into the user buffer)",
